@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""Benchmark: interactions/sec of the device reduction loop (BASELINE.json).
+
+Default workload (``--workload batch``): 4096 independent Ackermann(3,6) nets
+(BASELINE.json configs[4]), sharded contiguously over the ranks of a torchrun
+job (one GPU per rank, no data-path collective: ``scaling: strong`` — the total
+batch is fixed). A step reduces every net of the shard to normal form in one
+persistent-kernel launch. ``value`` = all nets' interactions / max-over-ranks
+device time (CUDA events around the launch, inputs resident in HBM, L2 flushed
+between steps). ``e2e`` = the same metric through the C ABI with host buffers:
+load (H2D), reduce, D2H of the results and the native host finalize, per step.
+
+Single-net configurations (A(3,10), A(3,8), fib(18)) are measured once each on
+rank 0 after the timed batch and reported under ``single_nets``; they do not
+shard (replicas only).
+
+``--impl reference`` times the reference algorithm on the host cores instead:
+the C++ restatement in oracle/ (the reference package is pure Python and
+cannot travel to the GPU box), with every host thread, on bounded samples.
+"""
+
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BATCH_NETS = 4096
+BATCH_PARAMS = (3, 6)
+GOLDEN_A36 = 344_964  # SURVEY.md §8(c), pinned by tests/test_oracle.py
+SINGLE = {
+    "A(3,10)": ("ackermann", (3, 10), 89_404_824),
+    "A(3,8)": ("ackermann", (3, 8), 5_574_030),
+    "fib(18)": ("fibonacci", (18,), 50_515),
+}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes: agent = 4 B label + 4 B per port,
+# equation = 8 B; interaction reads its equation and both agents and writes the
+# rhs equations and new agents; a communication merge moves 24 B.
+
+
+def rule_bytes(rules) -> list[int]:
+    from paper_1404_0076_b200.core import is_var
+
+    out = []
+    for rule in rules.rules.values():
+        rd = 8 + (4 + 4 * rule.lhs_a.arity) + (4 + 4 * rule.lhs_b.arity)
+        wr = 8 * len(rule.rhs)
+        for e in rule.rhs:
+            for side in (e.lhs, e.rhs):
+                work = [side]
+                while work:
+                    t = work.pop()
+                    if not is_var(t):
+                        wr += 4 + 4 * t.sym.arity
+                        work.extend(t.children)
+        out.append(rd + wr)
+    return out
+
+
+def algorithmic_bytes(rules, rule_counts, communications) -> int:
+    per = rule_bytes(rules)
+    return int(sum(int(c) * b for c, b in zip(rule_counts, per)) + 24 * int(communications))
+
+
+# ---------------------------------------------------------------------------
+
+
+def load_peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per launch from the committed ncu capture (profiles/), if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(workload)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_sample(program_name: str, params, seconds: float, threads: int) -> dict:
+    """Time the oracle (reference algorithm, C++ port) on the host for ~seconds."""
+    from oracle import oracle as O
+    from paper_1404_0076_b200.programs import program
+
+    prog = program(program_name)
+    rules = O.rules_for(program_name)
+    net = prog.build_input(*params)
+    deadline = time.perf_counter() + seconds
+    done = [0] * threads
+    ints = [0] * threads
+
+    def worker(k):
+        while time.perf_counter() < deadline or done[k] == 0:
+            r = O.run_config(net, rules, collect=False)
+            done[k] += 1
+            ints[k] += r.interactions
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(worker, range(threads)))
+    wall = time.perf_counter() - t0
+    return {"value": sum(ints) / wall, "nets": sum(done), "wall_s": wall, "interactions": sum(ints)}
+
+
+def run_reference(args) -> None:
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    name, params, wl = workload_spec(args.workload)
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(name, params, args.ref_seconds, threads)
+        if i >= args.warmup:
+            per_step.append(s)
+    total_i = sum(s["interactions"] for s in per_step)
+    total_t = sum(s["wall_s"] for s in per_step)
+    value = total_i / total_t
+    line = {
+        "impl": "reference",
+        "metric": "interactions/sec",
+        "value": value,
+        "unit": "interactions/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000 * total_t / len(per_step),
+        "higher_is_better": True,
+        "scaling": "strong" if args.workload == "batch" else "replicas",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (deterministic Ackermann/Fibonacci nets, no RNG)",
+        "config": wl,
+        "cpu_baseline": {
+            "value": value,
+            "unit": "interactions/s",
+            "cores": threads,
+            "kind": "port",
+            "sample": f"{sum(s['nets'] for s in per_step)} nets of {name}{params} over {args.steps} steps of "
+                      f"~{args.ref_seconds}s, oracle/inet_oracle.cpp (C++ restatement of "
+                      f"inet.engine.evaluate), one net per host thread",
+        },
+        "e2e": {"value": value, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_spec(name: str):
+    if name == "batch":
+        return "ackermann", BATCH_PARAMS, {"workload": f"batch {BATCH_NETS} x Ackermann(3,6)", "nets": BATCH_NETS,
+                                           "net": "A(3,6)", "l2": "flushed between steps (256 MiB write)"}
+    prog, params, _ = SINGLE[{"a310": "A(3,10)", "a38": "A(3,8)", "fib18": "fib(18)"}[name]]
+    label = {"a310": "A(3,10)", "a38": "A(3,8)", "fib18": "fib(18)"}[name]
+    return prog, params, {"workload": f"single net {label}", "nets": 1, "net": label,
+                          "l2": "flushed between steps (256 MiB write)"}
+
+
+def check_normal_forms(ctx, n_nets: int, height: int, sample: int = 64) -> None:
+    """Every sampled net must reduce to S^height(Z) with no residual equation."""
+    ctx.finalize(0xFFFFFFFF, 0)
+    step = max(1, n_nets // sample)
+    for i in range(0, n_nets, step):
+        agents, iface, eqs = ctx.result(i)
+        assert len(eqs) == 0 and len(iface) == 1 and len(agents) == height + 1, (i, len(agents), len(eqs))
+
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1404_0076_b200 import EngineConfig, _native, engine
+    from paper_1404_0076_b200.programs import ackermann_value, fibonacci_value, program
+
+    rank, local, world = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = local
+    name, params, wl = workload_spec(args.workload)
+    prog = program(name)
+    if args.workload == "batch":
+        lo, hi = rank * BATCH_NETS // world, (rank + 1) * BATCH_NETS // world
+        configs = [prog.build_input(*params) for _ in range(hi - lo)]
+        per_net = GOLDEN_A36
+    else:
+        configs = [prog.build_input(*params)]
+        per_net = SINGLE[wl["net"]][2]
+    n_nets = len(configs)
+    ecfg = EngineConfig(collect_stats=False, threads=args.threads)
+    prep = engine.prepare(configs, prog.rules)
+    ctx = _native.Context(dev)
+    ctx.load_rules(prep.blob)
+    ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
+    k = engine.native_cfg(ecfg)
+    k.count_rules = 1
+    code, _ = ctx.reduce(k)  # accounting + correctness run
+    assert code == _native.OK, _native.strerror(code)
+    ti, tc, max_rounds, nfail = ctx.totals()
+    assert nfail == 0 and ti == per_net * n_nets, (ti, per_net * n_nets)
+    counts = np.zeros(len(prog.rules.rules), dtype=np.uint64)
+    for i in range(n_nets):
+        counts += ctx.rule_counts(i, len(prog.rules.rules))
+    alg_bytes = algorithmic_bytes(prog.rules, counts, tc)
+    height = ackermann_value(*params) if name == "ackermann" else fibonacci_value(*params)
+    check_normal_forms(ctx, n_nets, height)
+    k.count_rules = 0
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{dev}")
+
+    def flush_l2():
+        flush.zero_()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush_l2()
+        ctx.rerun(k)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(dev) as clocks:
+        for _ in range(args.steps):
+            flush_l2()
+            times.append(ctx.rerun(k))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    my_ms = sum(times)
+    t = torch.tensor([my_ms], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    total_interactions = per_net * (BATCH_NETS if args.workload == "batch" else world)
+    value = total_interactions * args.steps / (max_ms / 1000.0)
+    kernel_ms = my_ms / args.steps
+
+    # e2e through the C ABI with host buffers (H2D, kernel, D2H, host finalize)
+    e2e_times = []
+    h2d = d2h = 0
+    for i in range(max(1, args.e2e_steps)):
+        t0 = time.perf_counter()
+        ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
+        code, _ = ctx.reduce(k)
+        ctx.finalize(0xFFFFFFFF, 0)
+        agents0, _, _ = ctx.result(0)
+        e2e_times.append(time.perf_counter() - t0)
+        assert code == _native.OK and len(agents0) == height + 1
+        h2d, d2h = ctx.io_bytes()
+    et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = total_interactions * len(e2e_times) / float(et.item())
+
+    peak, peak_kind = load_peaks()
+    achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9
+    line = None
+    if rank == 0:
+        info = ctx.info()
+        line = {
+            "metric": "interactions/sec",
+            "value": value,
+            "unit": "interactions/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong" if args.workload == "batch" else "replicas",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic (deterministic Ackermann nets built by paper_1404_0076_b200.programs, no RNG)",
+            "config": dict(wl, parallelism=f"dp{world} (nets sharded, no collective)",
+                           interactions_per_net=per_net, rounds_per_net=max_rounds,
+                           threads_per_net=engine.native_cfg(ecfg).threads or "auto"),
+            "e2e": {"value": e2e_value, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "path": "C ABI inet_batch_load+inet_batch_reduce+inet_batch_finalize, host flat buffers"},
+            "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "note": "SURVEY.md §8(d) bytes: per-rule (read+write) x device rule histogram "
+                                 "+ 24 B per communication"},
+            "clocks": clocks.summary(),
+            "device": info,
+        }
+    if world > 1:
+        dist.barrier()
+    # single nets (rank 0, N=1 headline for A(3,10)); replicas only
+    if rank == 0 and args.single:
+        singles = {}
+        for label, (pname, pparams, golden) in SINGLE.items():
+            p = program(pname)
+            pr = engine.prepare([p.build_input(*pparams)], p.rules)
+            c2 = _native.Context(dev)
+            c2.load_rules(pr.blob)
+            c2.load_batch(pr.agents, pr.agent_off, pr.eqs, pr.eq_off, pr.iface, pr.iface_off, pr.n_vars)
+            kk = engine.native_cfg(EngineConfig(collect_stats=False))
+            code, _ = c2.reduce(kk)
+            st = c2.stats(0)
+            assert code == _native.OK and st.interactions == golden, (label, st.interactions)
+            best = []
+            for _ in range(3):
+                flush_l2()
+                best.append(c2.rerun(kk))
+            ms = min(best)
+            singles[label] = {"interactions": golden, "rounds": st.rounds, "device_ms": ms,
+                              "interactions_per_s": golden / (ms / 1000.0),
+                              "us_per_round": 1000.0 * ms / max(st.rounds, 1)}
+            c2.close()
+        line["single_nets"] = singles
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        s = cpu_sample(name, params, args.cpu_seconds, threads)
+        line["cpu_baseline"] = {
+            "value": s["value"], "unit": "interactions/s", "cores": threads, "kind": "port",
+            "sample": f"{s['nets']} nets of {name}{params} in {s['wall_s']:.1f}s, oracle/inet_oracle.cpp "
+                      f"(C++ restatement of inet.engine.evaluate), one net per host thread",
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=["batch", "a310", "a38", "fib18"], default="batch")
+    ap.add_argument("--threads", type=int, default=0, help="CTA size per net (0 = auto)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single", dest="single", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,183 @@
+/*
+ * inet_b200.h — C ABI of the B200 interaction-net reducer.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   inet.engine.evaluate(config, rules, cfg) -> EvalResult
+ *   (/root/reference/pkg/src/inet/engine.py:186-228)
+ * and its helpers interaction_phase / communication_phase / reduce_by_key /
+ * finalize (engine.py:59-166, 287-362). The Python host module
+ * paper_1404_0076_b200.engine binds these entry points with ctypes; the
+ * reference-side binding a maintainer would add is shown in INTEGRATION.md.
+ *
+ * Everything is plain C: 32-bit words, host pointers and sizes. No CUDA or
+ * torch types cross the boundary.
+ *
+ * Flat formats
+ * ------------
+ * term ref   u32. Bit 31 set: variable, id = low 31 bits. Otherwise an index
+ *            into the agent array. INET_NONE (0xFFFFFFFF) = no term.
+ * agent      4 x u32 {label, port0, port1, port2}; unused ports INET_NONE.
+ *            (arity <= 3; every shipped program has arity <= 2.)
+ * equation   2 x u32 {lhs ref, rhs ref}.
+ * rule blob  see "Rule blob" below; built by
+ *            paper_1404_0076_b200.flat.compile_rules from a RuleSet
+ *            (the reference's Rule/RuleSet, core.py:158-251).
+ *
+ * Rule blob (u32 words)
+ * ---------------------
+ *   [0] INET_RULES_MAGIC  [1] n_labels (<= 64)  [2] n_rules (<= 256)  [3] 0
+ *   pair table: n_labels*n_labels u16 entries packed two per word,
+ *     entry[la*n_labels+lb] = 0xFFFF (no rule) or (rule << 1 | swap), where
+ *     swap means the equation's lhs plays the rule's lhs_b
+ *     (core.py:287-298: orientation of instantiate).
+ *   n_rules records of 16 words:
+ *     w0        n_new | n_eq << 8 | n_fresh << 16
+ *     w1..w8    new agent m: label | src0 << 8 | src1 << 16 | src2 << 24
+ *     w9..w12   rhs equation e: (srcL | srcR << 8) in 16-bit half (e & 1)
+ *               of word 9 + e/2
+ *   source codes: 0..2 port k of lhs_a, 3..5 port k of lhs_b,
+ *     6..13 fresh variable j (bound_vars order, core.py:195-204),
+ *     14..21 new agent m, 22 none.
+ */
+#ifndef INET_B200_H
+#define INET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define INET_NONE 0xFFFFFFFFu
+#define INET_VAR_BIT 0x80000000u
+#define INET_RULES_MAGIC 0x31524E49u /* "INR1" */
+#define INET_MAX_ARITY 3
+#define INET_MAX_LABELS 64
+#define INET_MAX_RULES 256
+#define INET_MAX_NEW 8
+#define INET_MAX_EQ 8
+#define INET_MAX_FRESH 8
+
+/* Status codes. Mirrors the reference's error classes (errors.py:46-65). */
+enum inet_status {
+  INET_OK = 0,
+  INET_ERR_NO_RULE = 1,      /* NoRuleForPair(a, b)       engine.py:92 / core.py:307-312 */
+  INET_ERR_LOOP_CAP = 2,     /* LoopCapExceeded(max)      engine.py:205-207 */
+  INET_ERR_ARENA = 3,        /* agent / variable / queue arena exhausted at max size */
+  INET_ERR_CUDA = 4,         /* CUDA runtime failure */
+  INET_ERR_ARG = 5,          /* bad argument / malformed blob */
+  INET_ERR_UNSUPPORTED = 6,  /* exceeds a device-engine limit */
+  INET_ERR_NO_DEVICE = 7,    /* no CUDA device visible */
+  INET_ERR_STATE = 8         /* call order violated (e.g. fetch before reduce) */
+};
+
+typedef struct inet_ctx inet_ctx;
+
+/* Knobs of one reduction; EngineConfig (engine.py:35-48) maps onto it. */
+typedef struct inet_cfg {
+  uint32_t max_loops;     /* LoopCapExceeded when round > max_loops */
+  uint32_t collect_stats; /* record per-round rows (LoopStats) */
+  uint32_t threads;       /* CTA size per net; 0 = auto */
+  uint32_t ctas_per_net;  /* 1 = one CTA per net; 0 = auto (large single nets use a cluster) */
+  uint32_t cap_agents;    /* initial per-net agent arena; 0 = auto (grows on overflow) */
+  uint32_t cap_vars;      /* initial per-net variable table; 0 = auto (grows on overflow) */
+  uint32_t max_retries;   /* arena doublings before INET_ERR_ARENA; 0 = default */
+  uint32_t count_rules;   /* per-rule interaction histogram (accounting runs only) */
+} inet_cfg;
+
+/* Per-net outcome. */
+typedef struct inet_net_stats {
+  uint64_t interactions;   /* EvalResult.total_interactions */
+  uint64_t communications; /* EvalResult.total_communications */
+  uint32_t rounds;         /* rounds incl. the trailing no-op round (= len(loops)) */
+  uint32_t status;         /* inet_status of this net */
+  uint32_t err_label_a;    /* NoRuleForPair labels, equation orientation */
+  uint32_t err_label_b;
+  uint32_t agent_hw;       /* arena high-water (agents ever addressed) */
+  uint32_t var_hw;         /* variable-table high-water */
+  uint32_t n_residual;     /* parked equations at the fixpoint (input of finalize) */
+  uint32_t cap_agents;     /* capacities the successful run used */
+  uint32_t cap_vars;
+  uint32_t reserved;
+} inet_net_stats;
+
+/* Context: one device, one stream, device buffers reused across calls. */
+int inet_ctx_create(int device, inet_ctx** out);
+void inet_ctx_destroy(inet_ctx* ctx);
+const char* inet_strerror(int status);
+/* Device properties for reporting: SM count and clock (kHz). */
+int inet_device_info(inet_ctx* ctx, int* sm_count, int* clock_khz, char* name, size_t name_len);
+
+/* Upload a compiled rule set (replaces RuleSet.lookup + instantiate tables). */
+int inet_rules_load(inet_ctx* ctx, const uint32_t* blob, size_t n_words);
+
+/*
+ * Load a batch of nets (n_nets >= 1). Net i owns
+ *   agents[4*agent_off[i] .. 4*agent_off[i+1])   its agents (local indices)
+ *   eqs[2*eq_off[i] .. 2*eq_off[i+1])             its equations
+ *   iface[iface_off[i] .. iface_off[i+1])         its interface refs (host only)
+ *   n_vars[i]                                     variables 0..n_vars[i]-1 in use
+ * All refs are net-local. Data is copied; the caller keeps ownership.
+ */
+int inet_batch_load(inet_ctx* ctx, uint32_t n_nets, const uint32_t* agents, const uint64_t* agent_off,
+                    const uint32_t* eqs, const uint64_t* eq_off, const uint32_t* iface,
+                    const uint64_t* iface_off, const uint32_t* n_vars);
+
+/*
+ * Reduce every loaded net to its fixpoint on the device: the whole
+ * interaction / communication loop runs inside one persistent kernel with no
+ * host synchronisation per round (replaces engine.py:204-223). Host buffers
+ * were copied by inet_batch_load; this call performs H2D, the kernel(s),
+ * overflow retries and the D2H of results. *device_ms is the CUDA-event time
+ * of the reduction kernel(s) of the final, successful attempt.
+ * Returns the first non-OK net status, or INET_OK.
+ */
+int inet_batch_reduce(inet_ctx* ctx, const inet_cfg* cfg, float* device_ms);
+
+/* Same, but only the device part (inputs already resident from a previous
+ * inet_batch_reduce of the same batch): re-initialise device state from the
+ * resident copy and run the kernel. For device-timed benchmarking. */
+int inet_batch_rerun(inet_ctx* ctx, const inet_cfg* cfg, float* device_ms);
+
+int inet_batch_stats(inet_ctx* ctx, uint32_t net, inet_net_stats* out);
+/* Interactions per rule of net i (needs cfg.count_rules); counts[n_rules]. */
+int inet_batch_rule_counts(inet_ctx* ctx, uint32_t net, uint64_t* counts, uint32_t n_rules);
+/* Host<->device bytes moved by the last inet_batch_reduce (inputs, results). */
+int inet_batch_io_bytes(inet_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
+/* Aggregate over all nets (sum of interactions/communications, max rounds). */
+int inet_batch_totals(inet_ctx* ctx, uint64_t* interactions, uint64_t* communications, uint32_t* max_rounds,
+                      uint32_t* n_failed);
+
+/* Per-round rows of net i: 4 words per round {interactions, communications,
+ * live_equations, elapsed_ns}. Two-call protocol: rows==NULL returns count. */
+int inet_batch_rounds(inet_ctx* ctx, uint32_t net, uint32_t* rows, uint32_t* n_rows);
+
+/*
+ * Sequential cleanup of net i (engine.py:287-362): splice every parked
+ * equation into the other occurrence of its variable, in the reference's
+ * queue order, then compact the reachable normal form. Runs on host threads
+ * (all nets in parallel when net == INET_NONE).
+ */
+int inet_batch_finalize(inet_ctx* ctx, uint32_t net, uint32_t n_threads);
+
+/* Normal form of net i after finalize: pointers stay valid until the next
+ * load/reduce/finalize on this context. Agents are in preorder (children
+ * after parents), refs are local to these arrays; variable ids are the
+ * device's (input ids 0..n_vars-1 are preserved, fresh ids >= n_vars). */
+int inet_batch_result(inet_ctx* ctx, uint32_t net, const uint32_t** agents, uint32_t* n_agents,
+                      const uint32_t** iface, uint32_t* n_iface, const uint32_t** eqs, uint32_t* n_eqs);
+
+/*
+ * Stand-alone finalize on caller buffers (engine.finalize's signature, flat):
+ * agents/iface/eqs are modified in place; alive[e] receives 1 for equations
+ * that survive. n_vars bounds variable ids.
+ */
+int inet_finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface, uint32_t* eqs,
+                       uint32_t n_eqs, uint32_t n_vars, uint8_t* alive);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INET_B200_H */

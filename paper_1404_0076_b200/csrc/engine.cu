@@ -1,0 +1,617 @@
+// engine.cu — kernels and the C ABI of libinetb200 (see include/inet_b200.h).
+//
+// Host side: a context owns one device, one stream and device buffers that
+// are grown (never shrunk) and reused across calls, so a repeated reduction
+// does no cudaMalloc. A batch of nets is laid out as per-net slabs of equal
+// capacity; one CTA reduces one net (device.cuh), the grid covers the batch.
+// If any net overflows its arena the batch is re-run with doubled capacity.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/inet_b200.h"
+#include "device.cuh"
+#include "host.h"
+
+using inetdev::NetCtl;
+using inetdev::NetDesc;
+
+namespace {
+
+constexpr uint32_t kScratchWords = 33;
+
+template <int kBlock>
+__global__ void __launch_bounds__(kBlock) reduce_kernel(const NetDesc* __restrict__ nets, uint32_t n_nets,
+                                                        const uint32_t* __restrict__ blob, uint32_t max_rounds) {
+  extern __shared__ uint32_t smem[];
+  __shared__ NetDesc sd;
+  __shared__ uint32_t scratch[kScratchWords];
+  const uint32_t n_labels = blob[1], n_rules = blob[2];
+  const uint32_t pair_words = (n_labels * n_labels + 1) / 2;
+  const uint32_t words = pair_words + n_rules * inetdev::kRuleWords;
+  for (uint32_t i = threadIdx.x; i < words; i += kBlock) smem[i] = blob[4 + i];
+  const uint16_t* pair = reinterpret_cast<const uint16_t*>(smem);
+  const uint32_t* rules = smem + pair_words;
+  for (uint32_t net = blockIdx.x; net < n_nets; net += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) sd = nets[net];
+    __syncthreads();
+    inetdev::run_net(sd, pair, rules, n_labels, max_rounds, scratch);
+  }
+}
+
+using KernelFn = void (*)(const NetDesc*, uint32_t, const uint32_t*, uint32_t);
+
+KernelFn pick_kernel(uint32_t threads) {
+  switch (threads) {
+    case 64:
+      return reduce_kernel<64>;
+    case 128:
+      return reduce_kernel<128>;
+    case 256:
+      return reduce_kernel<256>;
+    case 512:
+      return reduce_kernel<512>;
+    default:
+      return reduce_kernel<1024>;
+  }
+}
+
+uint32_t pow2_at_least(uint32_t v) {
+  uint32_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (cudaMalloc(&p, want) != cudaSuccess) return -1;
+    bytes = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+struct inet_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // rules
+  std::vector<uint32_t> blob;
+  DevBuf d_blob;
+  uint32_t n_labels = 0, n_rules = 0, smem_bytes = 0;
+  // batch input (host copies)
+  uint32_t n_nets = 0;
+  std::vector<uint32_t> agents, eqs, iface, n_vars;
+  std::vector<uint64_t> agent_off, eq_off, iface_off;
+  uint32_t max_in_agents = 0, max_in_eqs = 0, max_in_vars = 0;
+  bool input_resident = false;
+  // device state
+  DevBuf d_in_agents, d_in_eqs, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist;
+  bool count_rules = false;
+  std::vector<uint32_t> h_hist;
+  uint64_t io_h2d = 0, io_d2h = 0;
+  uint32_t cap_agents = 0, cap_vars = 0, cap_queue = 0, cap_rounds = 0, ring_a = 0, ring_v = 0;
+  bool collect_stats = false;
+  bool reduced = false;
+  // results (host)
+  std::vector<NetCtl> ctl;
+  std::vector<inet_net_stats> stats;
+  std::vector<uint32_t> h_agents;     // per-net slab prefixes [n_nets * agent_pitch * 4]
+  std::vector<uint32_t> h_resid;      // [n_nets * resid_pitch * 2]
+  uint32_t agent_pitch = 0, resid_pitch = 0;
+  std::vector<uint32_t> h_rounds;     // [n_nets * cap_rounds * 4]
+  std::vector<inethost::NormalForm> results;
+  std::vector<uint8_t> finalized;
+};
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess) {                                                                   \
+      std::fprintf(stderr, "inet_b200: %s failed: %s\n", #expr, cudaGetErrorString(_e));    \
+      return INET_ERR_CUDA;                                                                    \
+    }                                                                                          \
+  } while (0)
+
+extern "C" {
+
+const char* inet_strerror(int status) {
+  switch (status) {
+    case INET_OK:
+      return "ok";
+    case INET_ERR_NO_RULE:
+      return "no rule for active pair";
+    case INET_ERR_LOOP_CAP:
+      return "loop cap exceeded";
+    case INET_ERR_ARENA:
+      return "device arena exhausted";
+    case INET_ERR_CUDA:
+      return "CUDA runtime error";
+    case INET_ERR_ARG:
+      return "invalid argument";
+    case INET_ERR_UNSUPPORTED:
+      return "net or rule set exceeds a device-engine limit";
+    case INET_ERR_NO_DEVICE:
+      return "no CUDA device";
+    case INET_ERR_STATE:
+      return "call order violated";
+    default:
+      return "unknown status";
+  }
+}
+
+int inet_ctx_create(int device, inet_ctx** out) {
+  if (!out) return INET_ERR_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return INET_ERR_NO_DEVICE;
+  if (device < 0 || device >= n) return INET_ERR_ARG;
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new inet_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    delete c;
+    return INET_ERR_CUDA;
+  }
+  *out = c;
+  return INET_OK;
+}
+
+void inet_ctx_destroy(inet_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (DevBuf* b : {&c->d_blob, &c->d_in_agents, &c->d_in_eqs, &c->d_desc, &c->d_agents, &c->d_vslot, &c->d_aring,
+                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist})
+    b->release();
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int inet_device_info(inet_ctx* c, int* sm_count, int* clock_khz, char* name, size_t name_len) {
+  if (!c) return INET_ERR_ARG;
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, c->device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (clock_khz) cudaDeviceGetAttribute(clock_khz, cudaDevAttrClockRate, c->device);
+  if (name && name_len) {
+    std::strncpy(name, prop.name, name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  return INET_OK;
+}
+
+int inet_rules_load(inet_ctx* c, const uint32_t* blob, size_t n_words) {
+  if (!c || !blob || n_words < 4) return INET_ERR_ARG;
+  int st = inethost::validate_rule_blob(blob, n_words);
+  if (st != INET_OK) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->blob.assign(blob, blob + n_words);
+  c->n_labels = blob[1];
+  c->n_rules = blob[2];
+  c->smem_bytes = static_cast<uint32_t>((n_words - 4) * 4);
+  if (c->d_blob.ensure(n_words * 4)) return INET_ERR_CUDA;
+  CUDA_TRY(cudaMemcpyAsync(c->d_blob.p, blob, n_words * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return INET_OK;
+}
+
+int inet_batch_load(inet_ctx* c, uint32_t n_nets, const uint32_t* agents, const uint64_t* agent_off,
+                    const uint32_t* eqs, const uint64_t* eq_off, const uint32_t* iface, const uint64_t* iface_off,
+                    const uint32_t* n_vars) {
+  if (!c || n_nets == 0 || !agent_off || !eq_off || !iface_off || !n_vars) return INET_ERR_ARG;
+  if (c->blob.empty()) return INET_ERR_STATE;
+  c->n_nets = n_nets;
+  c->agent_off.assign(agent_off, agent_off + n_nets + 1);
+  c->eq_off.assign(eq_off, eq_off + n_nets + 1);
+  c->iface_off.assign(iface_off, iface_off + n_nets + 1);
+  c->n_vars.assign(n_vars, n_vars + n_nets);
+  c->agents.assign(agents, agents + 4 * agent_off[n_nets]);
+  c->eqs.assign(eqs, eqs + 2 * eq_off[n_nets]);
+  c->iface.assign(iface, iface + iface_off[n_nets]);
+  c->max_in_agents = c->max_in_eqs = c->max_in_vars = 0;
+  for (uint32_t i = 0; i < n_nets; ++i) {
+    const uint64_t na = agent_off[i + 1] - agent_off[i], ne = eq_off[i + 1] - eq_off[i];
+    if (na >= INET_VAR_BIT || ne >= INET_VAR_BIT || n_vars[i] >= INET_VAR_BIT - 1) return INET_ERR_UNSUPPORTED;
+    c->max_in_agents = std::max<uint32_t>(c->max_in_agents, static_cast<uint32_t>(na));
+    c->max_in_eqs = std::max<uint32_t>(c->max_in_eqs, static_cast<uint32_t>(ne));
+    c->max_in_vars = std::max<uint32_t>(c->max_in_vars, n_vars[i]);
+  }
+  int st = inethost::validate_nets(*c);
+  if (st != INET_OK) return st;
+  c->input_resident = false;
+  c->reduced = false;
+  c->results.clear();
+  c->finalized.clear();
+  return INET_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int upload_input(inet_ctx* c) {
+  const size_t na = c->agents.size() * 4, ne = c->eqs.size() * 4;
+  if (c->d_in_agents.ensure(std::max<size_t>(na, 16)) || c->d_in_eqs.ensure(std::max<size_t>(ne, 8)))
+    return INET_ERR_CUDA;
+  if (na) CUDA_TRY(cudaMemcpyAsync(c->d_in_agents.p, c->agents.data(), na, cudaMemcpyHostToDevice, c->stream));
+  if (ne) CUDA_TRY(cudaMemcpyAsync(c->d_in_eqs.p, c->eqs.data(), ne, cudaMemcpyHostToDevice, c->stream));
+  c->input_resident = true;
+  c->io_h2d += na + ne;
+  return INET_OK;
+}
+
+// Size the per-net slabs and write the descriptor table.
+int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_rounds) {
+  const uint32_t n = c->n_nets;
+  c->cap_agents = cap_agents;
+  c->cap_vars = cap_vars;
+  c->cap_queue = cap_agents / 2 + c->max_in_eqs + 1;
+  c->cap_rounds = cap_rounds;
+  c->ring_a = pow2_at_least(cap_agents);
+  c->ring_v = pow2_at_least(cap_vars);
+  const size_t N = n;
+  if (c->d_agents.ensure(N * cap_agents * 16) || c->d_vslot.ensure(N * cap_vars * 4) ||
+      c->d_aring.ensure(N * c->ring_a * 4) || c->d_vring.ensure(N * c->ring_v * 4) ||
+      c->d_queue.ensure(N * 2 * c->cap_queue * 8) || c->d_resid.ensure(N * cap_vars * 8) ||
+      c->d_ctl.ensure(N * sizeof(NetCtl)) || c->d_desc.ensure(N * sizeof(NetDesc)) ||
+      (cap_rounds && c->d_stats.ensure(N * cap_rounds * 16)) ||
+      (c->count_rules && c->d_hist.ensure(N * std::max(c->n_rules, 1u) * 4)))
+    return INET_ERR_CUDA;
+  if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * std::max(c->n_rules, 1u) * 4, c->stream));
+  std::vector<NetDesc> desc(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    NetDesc& d = desc[i];
+    std::memset(&d, 0, sizeof(d));
+    d.agents = static_cast<uint4*>(c->d_agents.p) + size_t(i) * cap_agents;
+    d.vslot = static_cast<uint32_t*>(c->d_vslot.p) + size_t(i) * cap_vars;
+    d.aring = static_cast<uint32_t*>(c->d_aring.p) + size_t(i) * c->ring_a;
+    d.vring = static_cast<uint32_t*>(c->d_vring.p) + size_t(i) * c->ring_v;
+    d.queue = static_cast<uint2*>(c->d_queue.p) + size_t(i) * 2 * c->cap_queue;
+    d.stats = cap_rounds ? static_cast<uint4*>(c->d_stats.p) + size_t(i) * cap_rounds : nullptr;
+    d.residual = static_cast<uint2*>(c->d_resid.p) + size_t(i) * cap_vars;
+    d.ctl = static_cast<NetCtl*>(c->d_ctl.p) + i;
+    d.rule_hist = c->count_rules ? static_cast<uint32_t*>(c->d_hist.p) + size_t(i) * std::max(c->n_rules, 1u) : nullptr;
+    d.cap_agents = cap_agents;
+    d.cap_vars = cap_vars;
+    d.cap_queue = c->cap_queue;
+    d.cap_rounds = cap_rounds;
+    d.amask = c->ring_a - 1;
+    d.vmask = c->ring_v - 1;
+    d.in_agents = static_cast<const uint4*>(c->d_in_agents.p) + c->agent_off[i];
+    d.in_eqs = static_cast<const uint2*>(c->d_in_eqs.p) + c->eq_off[i];
+    d.n_in_agents = static_cast<uint32_t>(c->agent_off[i + 1] - c->agent_off[i]);
+    d.n_in_eqs = static_cast<uint32_t>(c->eq_off[i + 1] - c->eq_off[i]);
+    d.n_in_vars = c->n_vars[i];
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_desc.p, desc.data(), N * sizeof(NetDesc), cudaMemcpyHostToDevice, c->stream));
+  return INET_OK;
+}
+
+uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
+  if (cfg && cfg->threads) {
+    uint32_t t = cfg->threads;
+    if (t <= 64) return 64;
+    if (t <= 128) return 128;
+    if (t <= 256) return 256;
+    if (t <= 512) return 512;
+    return 1024;
+  }
+  if (c->n_nets >= 2048) return 128;
+  if (c->n_nets >= 256) return 256;
+  return c->n_nets >= 16 ? 512 : 1024;
+}
+
+// One attempt at the current capacities: init + reduce kernel, timed.
+int launch(inet_ctx* c, const inet_cfg* cfg, float* ms) {
+  const uint32_t threads = auto_threads(c, cfg);
+  KernelFn fn = pick_kernel(threads);
+  if (c->smem_bytes > 48 * 1024) {
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(c->smem_bytes)));
+  }
+  const uint32_t max_rounds = cfg ? cfg->max_loops : 1000000u;
+  int dev_sms = 0;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), c->smem_bytes);
+  uint32_t grid = std::max(1, dev_sms * std::max(per_sm, 1));
+  grid = std::min(grid, c->n_nets);
+  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+  fn<<<grid, threads, c->smem_bytes, c->stream>>>(static_cast<const NetDesc*>(c->d_desc.p), c->n_nets,
+                                                  static_cast<const uint32_t*>(c->d_blob.p), max_rounds);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+  CUDA_TRY(cudaEventSynchronize(c->ev1));
+  CUDA_TRY(cudaEventElapsedTime(ms, c->ev0, c->ev1));
+  return INET_OK;
+}
+
+int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
+  if (!c || c->n_nets == 0 || c->blob.empty()) return INET_ERR_STATE;
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->input_resident) {
+    int st = upload_input(c);
+    if (st) return st;
+  }
+  const uint32_t max_loops = cfg ? cfg->max_loops : 1000000u;
+  c->collect_stats = cfg && cfg->collect_stats;
+  c->count_rules = cfg && cfg->count_rules;
+  uint32_t cap_rounds = 0;
+  if (c->collect_stats) cap_rounds = std::min<uint32_t>(max_loops + 1u, 1u << 22);
+  // initial capacities: enough for the inputs plus headroom
+  uint32_t ca = cfg && cfg->cap_agents ? cfg->cap_agents : 0;
+  uint32_t cv = cfg && cfg->cap_vars ? cfg->cap_vars : 0;
+  if (!ca) ca = c->n_nets == 1 ? (1u << 20) : 4096u;
+  if (!cv) cv = c->n_nets == 1 ? (1u << 20) : 8192u;
+  ca = std::max(ca, c->max_in_agents + 64);
+  cv = std::max(cv, c->max_in_vars + 64);
+  const uint32_t retries = cfg && cfg->max_retries ? cfg->max_retries : 8;
+  float ms = 0;
+  c->ctl.assign(c->n_nets, NetCtl{});
+  for (uint32_t attempt = 0;; ++attempt) {
+    int st = layout(c, ca, cv, cap_rounds);
+    if (st) return st;
+    st = launch(c, cfg, &ms);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpy(c->ctl.data(), c->d_ctl.p, c->n_nets * sizeof(NetCtl), cudaMemcpyDeviceToHost));
+    c->io_d2h += c->n_nets * sizeof(NetCtl);
+    c->io_h2d += c->n_nets * sizeof(NetDesc);
+    bool oom = false;
+    for (uint32_t i = 0; i < c->n_nets; ++i) oom |= c->ctl[i].err == INET_ERR_ARENA;
+    if (!oom || attempt + 1 >= retries) break;
+    // grow: agents and variables double (queue follows agents)
+    if (uint64_t(ca) * 2 >= INET_VAR_BIT || uint64_t(cv) * 2 >= INET_VAR_BIT) break;
+    ca *= 2;
+    cv *= 2;
+  }
+  if (device_ms) *device_ms = ms;
+  c->stats.assign(c->n_nets, inet_net_stats{});
+  int first = INET_OK;
+  for (uint32_t i = 0; i < c->n_nets; ++i) {
+    const NetCtl& k = c->ctl[i];
+    inet_net_stats& s = c->stats[i];
+    s.interactions = k.interactions;
+    s.communications = k.communications;
+    s.rounds = k.rounds;
+    s.status = k.err;
+    s.err_label_a = k.err_a;
+    s.err_label_b = k.err_b;
+    s.agent_hw = std::min(k.agent_bump, c->cap_agents);
+    s.var_hw = std::min(k.var_bump, c->cap_vars);
+    s.n_residual = k.n_residual;
+    s.cap_agents = c->cap_agents;
+    s.cap_vars = c->cap_vars;
+    if (first == INET_OK && k.err) first = static_cast<int>(k.err);
+  }
+  c->reduced = true;
+  c->results.assign(c->n_nets, inethost::NormalForm{});
+  c->finalized.assign(c->n_nets, 0);
+  if (fetch) {
+    // results: agent slabs up to the high-water, residual equations, round rows
+    uint32_t max_hw = 0, max_res = 0;
+    for (auto& s : c->stats) {
+      max_hw = std::max(max_hw, s.agent_hw);
+      max_res = std::max(max_res, s.n_residual);
+    }
+    // strided copies of each slab's used prefix
+    c->agent_pitch = std::max(max_hw, 1u);
+    c->resid_pitch = std::max(max_res, 1u);
+    c->h_agents.resize(size_t(c->n_nets) * c->agent_pitch * 4);
+    c->h_resid.resize(size_t(c->n_nets) * c->resid_pitch * 2);
+    if (max_hw)
+      CUDA_TRY(cudaMemcpy2DAsync(c->h_agents.data(), size_t(c->agent_pitch) * 16, c->d_agents.p,
+                                 size_t(c->cap_agents) * 16, size_t(max_hw) * 16, c->n_nets, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    if (max_res)
+      CUDA_TRY(cudaMemcpy2DAsync(c->h_resid.data(), size_t(c->resid_pitch) * 8, c->d_resid.p, size_t(c->cap_vars) * 8,
+                                 size_t(max_res) * 8, c->n_nets, cudaMemcpyDeviceToHost, c->stream));
+    if (c->collect_stats) {
+      uint32_t max_r = 0;
+      for (auto& s : c->stats) max_r = std::max(max_r, std::min(s.rounds, c->cap_rounds));
+      c->h_rounds.resize(size_t(c->n_nets) * c->cap_rounds * 4);
+      if (max_r)
+        CUDA_TRY(cudaMemcpy2DAsync(c->h_rounds.data(), size_t(c->cap_rounds) * 16, c->d_stats.p,
+                                   size_t(c->cap_rounds) * 16, size_t(max_r) * 16, c->n_nets,
+                                   cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (c->count_rules) {
+      c->h_hist.resize(size_t(c->n_nets) * std::max(c->n_rules, 1u));
+      CUDA_TRY(cudaMemcpyAsync(c->h_hist.data(), c->d_hist.p, c->h_hist.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->io_d2h += size_t(c->n_nets) * (size_t(max_hw) * 16 + size_t(max_res) * 8);
+    if (c->collect_stats) {
+      uint32_t max_r = 0;
+      for (auto& s : c->stats) max_r = std::max(max_r, std::min(s.rounds, c->cap_rounds));
+      c->io_d2h += size_t(c->n_nets) * max_r * 16;
+    }
+  }
+  return first;
+}
+
+}  // namespace
+
+extern "C" {
+
+int inet_batch_reduce(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
+  if (!c) return INET_ERR_ARG;
+  c->input_resident = false;
+  c->io_h2d = c->io_d2h = 0;
+  return run(c, cfg, device_ms, true);
+}
+
+int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
+  if (!c || !c->reduced) return INET_ERR_STATE;
+  // capacities of the successful run are reused: no retry growth expected
+  inet_cfg k = cfg ? *cfg : inet_cfg{1000000u, 0, 0, 0, 0, 0, 0, 0};
+  c->count_rules = k.count_rules != 0;
+  k.cap_agents = c->cap_agents;
+  k.cap_vars = c->cap_vars;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const uint32_t cap_rounds = (k.collect_stats) ? std::min<uint32_t>(k.max_loops + 1u, 1u << 22) : 0;
+  int st = layout(c, c->cap_agents, c->cap_vars, cap_rounds);
+  if (st) return st;
+  float ms = 0;
+  st = launch(c, &k, &ms);
+  if (st) return st;
+  if (device_ms) *device_ms = ms;
+  return INET_OK;
+}
+
+int inet_batch_stats(inet_ctx* c, uint32_t net, inet_net_stats* out) {
+  if (!c || !out) return INET_ERR_ARG;
+  if (!c->reduced) return INET_ERR_STATE;
+  if (net >= c->n_nets) return INET_ERR_ARG;
+  *out = c->stats[net];
+  return INET_OK;
+}
+
+int inet_batch_rule_counts(inet_ctx* c, uint32_t net, uint64_t* counts, uint32_t n_rules) {
+  if (!c || !counts) return INET_ERR_ARG;
+  if (!c->reduced || !c->count_rules || c->h_hist.empty()) return INET_ERR_STATE;
+  if (net >= c->n_nets) return INET_ERR_ARG;
+  const uint32_t R = std::max(c->n_rules, 1u);
+  for (uint32_t r = 0; r < n_rules; ++r) counts[r] = r < c->n_rules ? c->h_hist[size_t(net) * R + r] : 0;
+  return INET_OK;
+}
+
+int inet_batch_io_bytes(inet_ctx* c, uint64_t* h2d, uint64_t* d2h) {
+  if (!c) return INET_ERR_ARG;
+  if (h2d) *h2d = c->io_h2d;
+  if (d2h) *d2h = c->io_d2h;
+  return INET_OK;
+}
+
+int inet_batch_totals(inet_ctx* c, uint64_t* interactions, uint64_t* communications, uint32_t* max_rounds,
+                      uint32_t* n_failed) {
+  if (!c) return INET_ERR_ARG;
+  if (!c->reduced) return INET_ERR_STATE;
+  uint64_t ti = 0, tc = 0;
+  uint32_t mr = 0, nf = 0;
+  for (auto& s : c->stats) {
+    ti += s.interactions;
+    tc += s.communications;
+    mr = std::max(mr, s.rounds);
+    nf += s.status != INET_OK;
+  }
+  if (interactions) *interactions = ti;
+  if (communications) *communications = tc;
+  if (max_rounds) *max_rounds = mr;
+  if (n_failed) *n_failed = nf;
+  return INET_OK;
+}
+
+int inet_batch_rounds(inet_ctx* c, uint32_t net, uint32_t* rows, uint32_t* n_rows) {
+  if (!c || !n_rows) return INET_ERR_ARG;
+  if (!c->reduced) return INET_ERR_STATE;
+  if (net >= c->n_nets) return INET_ERR_ARG;
+  if (!c->collect_stats) {
+    *n_rows = 0;
+    return INET_OK;
+  }
+  const uint32_t n = std::min(c->stats[net].rounds, c->cap_rounds);
+  if (!rows) {
+    *n_rows = n;
+    return INET_OK;
+  }
+  const uint32_t m = std::min(n, *n_rows);
+  std::memcpy(rows, c->h_rounds.data() + size_t(net) * c->cap_rounds * 4, size_t(m) * 16);
+  *n_rows = m;
+  return INET_OK;
+}
+
+int inet_batch_finalize(inet_ctx* c, uint32_t net, uint32_t n_threads) {
+  if (!c) return INET_ERR_ARG;
+  if (!c->reduced) return INET_ERR_STATE;
+  return inethost::finalize_batch(*c, net, n_threads);
+}
+
+int inet_batch_result(inet_ctx* c, uint32_t net, const uint32_t** agents, uint32_t* n_agents, const uint32_t** iface,
+                      uint32_t* n_iface, const uint32_t** eqs, uint32_t* n_eqs) {
+  if (!c) return INET_ERR_ARG;
+  if (!c->reduced || net >= c->n_nets || !c->finalized[net]) return INET_ERR_STATE;
+  const inethost::NormalForm& nf = c->results[net];
+  if (agents) *agents = nf.agents.data();
+  if (n_agents) *n_agents = static_cast<uint32_t>(nf.agents.size() / 4);
+  if (iface) *iface = nf.iface.data();
+  if (n_iface) *n_iface = static_cast<uint32_t>(nf.iface.size());
+  if (eqs) *eqs = nf.eqs.data();
+  if (n_eqs) *n_eqs = static_cast<uint32_t>(nf.eqs.size() / 2);
+  return INET_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// glue used by host.cpp (kept here because it needs the ctx layout)
+
+namespace inethost {
+
+int validate_nets(const inet_ctx& c) {
+  const uint32_t L = c.n_labels;
+  for (uint32_t i = 0; i < c.n_nets; ++i) {
+    const uint64_t a0 = c.agent_off[i], a1 = c.agent_off[i + 1];
+    const uint32_t na = static_cast<uint32_t>(a1 - a0), nv = c.n_vars[i];
+    auto ok_ref = [&](uint32_t r) {
+      if (r == INET_NONE) return false;
+      if (r & INET_VAR_BIT) return (r & ~INET_VAR_BIT) < nv;
+      return r < na;
+    };
+    for (uint64_t a = a0; a < a1; ++a) {
+      const uint32_t* rec = &c.agents[4 * a];
+      if (rec[0] >= L) return INET_ERR_UNSUPPORTED;
+      for (int k = 1; k < 4; ++k)
+        if (rec[k] != INET_NONE && !ok_ref(rec[k])) return INET_ERR_ARG;
+    }
+    for (uint64_t e = c.eq_off[i]; e < c.eq_off[i + 1]; ++e)
+      if (!ok_ref(c.eqs[2 * e]) || !ok_ref(c.eqs[2 * e + 1])) return INET_ERR_ARG;
+    for (uint64_t k = c.iface_off[i]; k < c.iface_off[i + 1]; ++k)
+      if (!ok_ref(c.iface[k])) return INET_ERR_ARG;
+  }
+  return INET_OK;
+}
+
+int finalize_batch(inet_ctx& c, uint32_t net, uint32_t n_threads) {
+  auto one = [&](uint32_t i) -> int {
+    const inet_net_stats& s = c.stats[i];
+    if (s.status != INET_OK) return static_cast<int>(s.status);
+    NetView v;
+    v.agents = c.h_agents.data() + size_t(i) * c.agent_pitch * 4;
+    v.n_agents = s.agent_hw;
+    v.residual = c.h_resid.data() + size_t(i) * c.resid_pitch * 2;
+    v.n_residual = s.n_residual;
+    v.iface = c.iface.data() + c.iface_off[i];
+    v.n_iface = static_cast<uint32_t>(c.iface_off[i + 1] - c.iface_off[i]);
+    v.n_vars = s.var_hw;
+    int st = finalize_net(v, c.results[i]);
+    if (st == INET_OK) c.finalized[i] = 1;
+    return st;
+  };
+  if (net != INET_NONE) {
+    if (net >= c.n_nets) return INET_ERR_ARG;
+    return one(net);
+  }
+  return parallel_for(c.n_nets, n_threads, one);
+}
+
+}  // namespace inethost

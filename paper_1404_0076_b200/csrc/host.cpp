@@ -1,0 +1,278 @@
+// host.cpp — sequential cleanup of a reduced net on flat arrays.
+//
+// finalize_flat restates engine.finalize (src/inet/engine.py:287-362): after
+// the device loop stops, the remaining equations are parked var-headed
+// equations whose variable's other occurrence is nested (inside an agent) or
+// in the interface. Every such equation x = t is eliminated by writing t into
+// the other occurrence of x, in the reference's queue order (equations in
+// order; an equation whose top-level slot received a term is re-queued).
+// An equation is kept when the other occurrence of x lies inside the
+// equation itself (a cycle, or x = x).
+//
+// The reference decides "inside the equation itself" with a DFS of the other
+// side (engine.py:275-284, 337). Here each agent carries the container it was
+// found in and containers are merged with union-find when a term is spliced,
+// so the test is O(alpha) instead of O(term size) and the whole pass is linear
+// even for an 8,190-deep Ackermann(3,10) result chain in any order.
+#include "host.h"
+
+#include <algorithm>
+#include <atomic>
+#include <deque>
+#include <thread>
+
+namespace inethost {
+
+namespace {
+
+constexpr uint32_t kNone = INET_NONE;
+constexpr uint32_t kVar = INET_VAR_BIT;
+
+inline bool is_var(uint32_t r) { return r != kNone && (r & kVar); }
+
+struct Finalizer {
+  uint32_t* ag;  // 4 words per agent
+  uint32_t na;
+  uint32_t* ifc;
+  uint32_t ni;
+  uint32_t* eq;  // 2 words per equation
+  uint32_t ne;
+  uint32_t nv;
+  // cells: [0,ni) interface, [ni, ni+2ne) equation sides, then 3 ports per agent
+  std::vector<uint32_t> occ;     // 2 cells per variable
+  std::vector<uint32_t> owner;   // container of each agent
+  std::vector<uint32_t> parent;  // union-find over containers [0, ni+ne)
+  std::vector<uint8_t> alive;
+
+  uint32_t eq_cell(uint32_t e, uint32_t s) const { return ni + 2 * e + s; }
+  uint32_t port_cell(uint32_t a, uint32_t k) const { return ni + 2 * ne + 3 * a + k; }
+  bool is_eq_cell(uint32_t c) const { return c >= ni && c < ni + 2 * ne; }
+  bool is_port_cell(uint32_t c) const { return c >= ni + 2 * ne; }
+  uint32_t& cell(uint32_t c) {
+    if (c < ni) return ifc[c];
+    if (c < ni + 2 * ne) return eq[c - ni];
+    const uint32_t p = c - ni - 2 * ne;
+    return ag[4 * (p / 3) + 1 + p % 3];
+  }
+  uint32_t find(uint32_t k) {
+    while (parent[k] != k) {
+      parent[k] = parent[parent[k]];
+      k = parent[k];
+    }
+    return k;
+  }
+  uint32_t container_of(uint32_t c) {
+    if (c < ni) return c;
+    if (c < ni + 2 * ne) return ni + (c - ni) / 2;
+    return find(owner[(c - ni - 2 * ne) / 3]);
+  }
+
+  // Record occurrences and owners below one root cell.
+  int scan(uint32_t root_cell, uint32_t container) {
+    std::vector<uint32_t> stack{root_cell};
+    while (!stack.empty()) {
+      const uint32_t c = stack.back();
+      stack.pop_back();
+      const uint32_t t = cell(c);
+      if (t == kNone) continue;
+      if (t & kVar) {
+        const uint32_t x = t & ~kVar;
+        if (x >= nv) return INET_ERR_ARG;
+        if (occ[2 * x] == kNone)
+          occ[2 * x] = c;
+        else if (occ[2 * x + 1] == kNone)
+          occ[2 * x + 1] = c;
+        else
+          return INET_ERR_ARG;  // name discipline broken (NameDisciplineError)
+        continue;
+      }
+      if (t >= na) return INET_ERR_ARG;
+      if (owner[t] != kNone) return INET_ERR_ARG;  // shared agent: not a tree
+      owner[t] = container;
+      for (uint32_t k = 0; k < 3; ++k)
+        if (ag[4 * t + 1 + k] != kNone) stack.push_back(port_cell(t, k));
+    }
+    return INET_OK;
+  }
+
+  int run() {
+    occ.assign(size_t(nv) * 2, kNone);
+    owner.assign(na, kNone);
+    parent.resize(ni + ne);
+    for (uint32_t k = 0; k < ni + ne; ++k) parent[k] = k;
+    alive.assign(ne, 1);
+    for (uint32_t i = 0; i < ni; ++i)
+      if (int st = scan(i, i)) return st;
+    for (uint32_t e = 0; e < ne; ++e)
+      for (uint32_t s = 0; s < 2; ++s)
+        if (int st = scan(eq_cell(e, s), ni + e)) return st;
+
+    std::deque<uint32_t> queue;
+    for (uint32_t e = 0; e < ne; ++e) queue.push_back(e);
+    while (!queue.empty()) {
+      const uint32_t e = queue.front();
+      queue.pop_front();
+      if (!alive[e]) continue;
+      for (uint32_t side = 0; side < 2; ++side) {
+        const uint32_t v = eq[2 * e + side];
+        if (!is_var(v)) continue;
+        const uint32_t x = v & ~kVar;
+        const uint32_t self = eq_cell(e, side);
+        uint32_t target = kNone;
+        for (uint32_t j = 0; j < 2; ++j) {
+          const uint32_t o = occ[2 * x + j];
+          if (o == kNone || o == self) continue;
+          if (is_eq_cell(o) && !alive[(o - ni) / 2]) continue;  // stale slot of a consumed equation
+          target = o;
+          break;
+        }
+        if (target == kNone) continue;
+        // the other occurrence must not be inside this very equation
+        if (target == eq_cell(e, 1 - side)) continue;
+        if (is_port_cell(target) && container_of(target) == ni + e) continue;
+        const uint32_t rep = eq[2 * e + 1 - side];
+        alive[e] = 0;
+        cell(target) = rep;
+        if (is_var(rep)) {
+          const uint32_t y = rep & ~kVar;
+          for (uint32_t j = 0; j < 2; ++j)
+            if (occ[2 * y + j] == eq_cell(e, 1 - side)) occ[2 * y + j] = target;
+        } else {
+          parent[ni + e] = container_of(target);
+        }
+        occ[2 * x] = occ[2 * x + 1] = kNone;
+        if (is_eq_cell(target)) {
+          const uint32_t f = (target - ni) / 2;
+          if (alive[f]) queue.push_back(f);
+        }
+        break;
+      }
+    }
+    return INET_OK;
+  }
+};
+
+}  // namespace
+
+int validate_rule_blob(const uint32_t* blob, size_t n_words) {
+  if (blob[0] != INET_RULES_MAGIC) return INET_ERR_ARG;
+  const uint32_t L = blob[1], R = blob[2];
+  if (L == 0 || L > INET_MAX_LABELS || R > INET_MAX_RULES) return INET_ERR_UNSUPPORTED;
+  const size_t pair_words = (size_t(L) * L + 1) / 2;
+  if (n_words != 4 + pair_words + size_t(R) * 16) return INET_ERR_ARG;
+  const uint16_t* pair = reinterpret_cast<const uint16_t*>(blob + 4);
+  for (size_t i = 0; i < size_t(L) * L; ++i)
+    if (pair[i] != 0xFFFFu && (pair[i] >> 1) >= R) return INET_ERR_ARG;
+  const uint32_t* rules = blob + 4 + pair_words;
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint32_t* w = rules + 16 * r;
+    const uint32_t nn = w[0] & 0xFF, ne = (w[0] >> 8) & 0xFF, nf = (w[0] >> 16) & 0xFF;
+    if (nn > INET_MAX_NEW || ne > INET_MAX_EQ || nf > INET_MAX_FRESH) return INET_ERR_UNSUPPORTED;
+    auto src_ok = [&](uint32_t s) {
+      if (s < 6) return true;
+      if (s < 14) return s - 6 < nf;
+      if (s < 22) return s - 14 < nn;
+      return s == 22;
+    };
+    for (uint32_t m = 0; m < nn; ++m) {
+      if ((w[1 + m] & 0xFF) >= L) return INET_ERR_ARG;
+      for (int k = 1; k < 4; ++k)
+        if (!src_ok((w[1 + m] >> (8 * k)) & 0xFF)) return INET_ERR_ARG;
+    }
+    for (uint32_t e = 0; e < ne; ++e) {
+      const uint32_t h = (w[9 + e / 2] >> ((e & 1) * 16)) & 0xFFFF;
+      if (!src_ok(h & 0xFF) || !src_ok(h >> 8) || (h & 0xFF) == 22 || (h >> 8) == 22) return INET_ERR_ARG;
+    }
+  }
+  return INET_OK;
+}
+
+int finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface, uint32_t* eqs,
+                  uint32_t n_eqs, uint32_t n_vars, uint8_t* alive) {
+  Finalizer f{agents, n_agents, iface, n_iface, eqs, n_eqs, n_vars, {}, {}, {}, {}};
+  int st = f.run();
+  if (st) return st;
+  if (alive) std::copy(f.alive.begin(), f.alive.end(), alive);
+  return INET_OK;
+}
+
+int finalize_net(const NetView& v, NormalForm& out) {
+  std::vector<uint32_t> ag(v.agents, v.agents + size_t(v.n_agents) * 4);
+  std::vector<uint32_t> ifc(v.iface, v.iface + v.n_iface);
+  std::vector<uint32_t> eq(v.residual, v.residual + size_t(v.n_residual) * 2);
+  Finalizer f{ag.data(), v.n_agents, ifc.data(), v.n_iface, eq.data(), v.n_residual, v.n_vars, {}, {}, {}, {}};
+  int st = f.run();
+  if (st) return st;
+  // compact the reachable normal form in preorder
+  std::vector<uint32_t> remap(v.n_agents, kNone);
+  std::vector<uint32_t> order;
+  std::vector<uint32_t> stack;
+  auto visit = [&](uint32_t root) {
+    if (root == kNone || (root & kVar)) return;
+    stack.push_back(root);
+    while (!stack.empty()) {
+      const uint32_t a = stack.back();
+      stack.pop_back();
+      remap[a] = static_cast<uint32_t>(order.size());
+      order.push_back(a);
+      for (int k = 2; k >= 0; --k) {
+        const uint32_t t = ag[4 * a + 1 + k];
+        if (t != kNone && !(t & kVar)) stack.push_back(t);
+      }
+    }
+  };
+  for (uint32_t i = 0; i < v.n_iface; ++i) visit(ifc[i]);
+  for (uint32_t e = 0; e < v.n_residual; ++e)
+    if (f.alive[e]) {
+      visit(eq[2 * e]);
+      visit(eq[2 * e + 1]);
+    }
+  auto map_ref = [&](uint32_t t) { return (t == kNone || (t & kVar)) ? t : remap[t]; };
+  out.agents.resize(order.size() * 4);
+  for (size_t j = 0; j < order.size(); ++j) {
+    const uint32_t a = order[j];
+    out.agents[4 * j] = ag[4 * a];
+    for (int k = 1; k < 4; ++k) out.agents[4 * j + k] = map_ref(ag[4 * a + k]);
+  }
+  out.iface.resize(v.n_iface);
+  for (uint32_t i = 0; i < v.n_iface; ++i) out.iface[i] = map_ref(ifc[i]);
+  out.eqs.clear();
+  for (uint32_t e = 0; e < v.n_residual; ++e)
+    if (f.alive[e]) {
+      out.eqs.push_back(map_ref(eq[2 * e]));
+      out.eqs.push_back(map_ref(eq[2 * e + 1]));
+    }
+  return INET_OK;
+}
+
+int parallel_for(uint32_t n, uint32_t n_threads, const std::function<int(uint32_t)>& fn) {
+  if (n_threads == 0) n_threads = std::max(1u, std::thread::hardware_concurrency());
+  n_threads = std::min(n_threads, n);
+  std::atomic<uint32_t> next{0};
+  std::atomic<int> first{INET_OK};
+  auto worker = [&]() {
+    for (;;) {
+      const uint32_t i = next.fetch_add(1);
+      if (i >= n) return;
+      const int st = fn(i);
+      int expect = INET_OK;
+      if (st != INET_OK) first.compare_exchange_strong(expect, st);
+    }
+  };
+  if (n_threads <= 1) {
+    worker();
+  } else {
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < n_threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+  }
+  return first.load();
+}
+
+}  // namespace inethost
+
+extern "C" int inet_finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface,
+                                  uint32_t* eqs, uint32_t n_eqs, uint32_t n_vars, uint8_t* alive) {
+  if ((n_agents && !agents) || (n_iface && !iface) || (n_eqs && !eqs)) return INET_ERR_ARG;
+  return inethost::finalize_flat(agents, n_agents, iface, n_iface, eqs, n_eqs, n_vars, alive);
+}

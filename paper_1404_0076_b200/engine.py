@@ -1,0 +1,393 @@
+"""Drop-in ``evaluate`` running the reduction loop on a B200.
+
+``evaluate(config, rules, cfg)`` has the reference's signature and result
+type (src/inet/engine.py:186-228): it validates ``slot_count`` on the host,
+flattens the net, compiles the rule table, and calls the C ABI
+(include/inet_b200.h) which runs the whole interaction/communication loop in
+one persistent CUDA kernel, then performs the sequential cleanup (finalize,
+engine.py:287-362) natively on the host and rebuilds terms of the caller's
+own classes.
+
+``evaluate_batch`` reduces many independent nets in one launch (one CTA per
+net). ``evaluate_sharded`` splits a batch over several GPUs, one host thread
+and one context per device, with no inter-GPU traffic.
+
+There is no CPU fallback: without the shared library or a CUDA device the
+calls raise ``DeviceError``.
+"""
+
+from __future__ import annotations
+
+import importlib
+import threading
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence, TypeVar
+
+import numpy as np
+
+from . import _native
+from .core import Configuration, Equation, RuleSet, Term, is_var, iter_vars
+from .errors import (
+    ArenaExhausted,
+    DeviceError,
+    LoopCapExceeded,
+    NameDisciplineError,
+    NoRuleForPair,
+    SlotOverflow,
+)
+from .flat import FlatNet, Labels, compile_rules, flatten, term_classes, unflatten
+from .profile import LoopStats
+
+T = TypeVar("T")
+
+
+@dataclass(slots=True)
+class EngineConfig:
+    """Same fields and defaults as the reference (engine.py:35-48).
+
+    ``worker_hint`` is accepted for compatibility; the device decides its own
+    parallelism. ``device`` selects the GPU; ``threads`` the CTA size per net
+    (0 = auto).
+    """
+
+    slot_count: Optional[int] = None
+    max_loops: int = 1_000_000
+    worker_hint: int = 1
+    collect_stats: bool = True
+    validate_phases: bool = False
+    device: int = 0
+    threads: int = 0
+
+
+@dataclass(slots=True)
+class EvalResult:
+    final: Configuration
+    loops: list[LoopStats]
+    total_interactions: int
+    total_communications: int
+
+
+def reduce_by_key(items: Sequence[T], key: Callable[[T], object], merge: Callable[[T, T], T]) -> list[T]:
+    """Fold adjacent equal-key items (engine.py:59-74); ``[2,0,3,3,3,7,5,5]`` -> ``[2,0,9,7,10]``.
+
+    Kept as a host utility of the API surface; the device engine replaces the
+    sort + reduce_by_key pass by variable-slot exchange.
+    """
+    out: list[T] = []
+    sentinel = last = object()
+    for x in items:
+        k = key(x)
+        if out and last is not sentinel and k == last:
+            out[-1] = merge(out[-1], x)
+        else:
+            out.append(x)
+            last = k
+    return out
+
+
+def check_name_discipline(interface: Sequence[Term], eqs: Sequence[Equation]) -> None:
+    """NameDisciplineError if some variable occurs more than twice (engine.py:169-183)."""
+    seen: dict[int, int] = {}
+    terms = list(interface) + [s for e in eqs for s in (e.lhs, e.rhs)]
+    for t in terms:
+        for v in iter_vars(t):
+            n = seen.get(v, 0) + 1
+            if n > 2:
+                raise NameDisciplineError(f"variable {v} occurs more than twice")
+            seen[v] = n
+
+
+# ---------------------------------------------------------------------------
+# error mapping
+
+
+def _errors_for(config):
+    """The caller's errors module (reference objects get reference exceptions)."""
+    mod = type(config).__module__
+    pkg = mod.rsplit(".", 1)[0] if "." in mod else None
+    if pkg and pkg != __name__.rsplit(".", 1)[0]:
+        try:
+            return importlib.import_module(pkg + ".errors")
+        except ImportError:
+            pass
+    from . import errors
+
+    return errors
+
+
+def _raise_status(code: int, st, labels: Labels, cfg: EngineConfig, errs) -> None:
+    if code == _native.NO_RULE:
+        a = labels.symbols[st.err_label_a].name
+        b = labels.symbols[st.err_label_b].name
+        raise getattr(errs, "NoRuleForPair", NoRuleForPair)(a, b)
+    if code == _native.LOOP_CAP:
+        raise getattr(errs, "LoopCapExceeded", LoopCapExceeded)(cfg.max_loops)
+    if code == _native.ARENA:
+        raise ArenaExhausted(
+            f"device arena exhausted at {st.cap_agents} agents / {st.cap_vars} variables per net"
+        )
+    raise DeviceError(code, _native.strerror(code))
+
+
+def _loop_stats_class(config):
+    mod = type(config).__module__
+    pkg = mod.rsplit(".", 1)[0] if "." in mod else None
+    if pkg and pkg != __name__.rsplit(".", 1)[0]:
+        try:
+            return importlib.import_module(pkg + ".profile").LoopStats
+        except (ImportError, AttributeError):
+            pass
+    return LoopStats
+
+
+def _result_class(config):
+    mod = type(config).__module__
+    pkg = mod.rsplit(".", 1)[0] if "." in mod else None
+    if pkg and pkg != __name__.rsplit(".", 1)[0]:
+        try:
+            return importlib.import_module(pkg + ".engine").EvalResult
+        except (ImportError, AttributeError):
+            pass
+    return EvalResult
+
+
+# ---------------------------------------------------------------------------
+# batch plumbing
+
+
+@dataclass
+class Prepared:
+    labels: Labels
+    blob: np.ndarray
+    flats: list
+    agents: np.ndarray
+    agent_off: np.ndarray
+    eqs: np.ndarray
+    eq_off: np.ndarray
+    iface: np.ndarray
+    iface_off: np.ndarray
+    n_vars: np.ndarray
+
+
+_blob_cache: dict = {}
+
+
+def prepare(configs: Sequence[Configuration], rules: RuleSet) -> Prepared:
+    """Flatten nets and compile the rule table (host work, no device)."""
+    labels = Labels.of(rules)
+    flats = [flatten(c, labels) for c in configs]  # may add config-only symbols
+    blob = compile_rules(rules, labels)
+    cat = lambda arrs, w: (np.concatenate([a.reshape(-1, w) for a in arrs]) if arrs else np.zeros((0, w), np.uint32))
+    offs = lambda arrs: np.concatenate([[0], np.cumsum([len(a) for a in arrs])]).astype(np.uint64)
+    return Prepared(
+        labels=labels,
+        blob=blob,
+        flats=flats,
+        agents=cat([f.agents for f in flats], 4),
+        agent_off=offs([f.agents for f in flats]),
+        eqs=cat([f.eqs for f in flats], 2),
+        eq_off=offs([f.eqs for f in flats]),
+        iface=np.concatenate([f.iface for f in flats]) if flats else np.zeros(0, np.uint32),
+        iface_off=offs([f.iface for f in flats]),
+        n_vars=np.array([len(f.var_ids) for f in flats], dtype=np.uint32),
+    )
+
+
+def native_cfg(cfg: EngineConfig) -> _native.Cfg:
+    k = _native.Cfg()
+    k.max_loops = max(0, min(int(cfg.max_loops), 0xFFFFFFFE))
+    k.collect_stats = 1 if cfg.collect_stats else 0
+    k.threads = cfg.threads
+    return k
+
+
+def run_prepared(ctx: _native.Context, prep: Prepared, cfg: EngineConfig) -> tuple[int, float]:
+    ctx.load_rules(prep.blob, key=prep.blob.tobytes())
+    ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
+    return ctx.reduce(native_cfg(cfg))
+
+
+def evaluate(config: Configuration, rules: RuleSet, cfg: Optional[EngineConfig] = None) -> EvalResult:
+    """Reduce ``config`` to normal form on the GPU (engine.py:186-228)."""
+    cfg = cfg if cfg is not None else EngineConfig()
+    errs = _errors_for(config)
+    if cfg.slot_count is not None and cfg.slot_count < rules.max_rhs_size:
+        raise getattr(errs, "SlotOverflow", SlotOverflow)(
+            f"slot_count {cfg.slot_count} is smaller than the largest rule rhs ({rules.max_rhs_size})"
+        )
+    if cfg.validate_phases:
+        check_name_discipline(config.interface, config.equations)
+    ctx = _native.context(getattr(cfg, "device", 0))
+    prep = prepare([config], rules)
+    with ctx.lock:
+        code, _ms = run_prepared(ctx, prep, cfg)
+        st = ctx.stats(0)
+        if code != _native.OK:
+            _raise_status(code, st, prep.labels, cfg, errs)
+        ctx.finalize(0, 1)
+        agents, iface, eqs = ctx.result(0)
+        rows = ctx.rounds(0) if cfg.collect_stats else None
+    final = unflatten(agents, iface, eqs, prep.labels, prep.flats[0], term_classes(config))
+    if cfg.validate_phases:
+        check_name_discipline(final.interface, final.equations)
+    loops = []
+    if rows is not None:
+        LS = _loop_stats_class(config)
+        loops = [LS(i + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for i, r in enumerate(rows)]
+    return _result_class(config)(final, loops, int(st.interactions), int(st.communications))
+
+
+@dataclass
+class BatchResult:
+    """Outcome of ``evaluate_batch``: per-net results plus device timing."""
+
+    results: list  # EvalResult per net (final is None when as_terms=False)
+    device_ms: float
+    total_interactions: int
+    total_communications: int
+    max_rounds: int
+
+
+def evaluate_batch(
+    configs: Sequence[Configuration],
+    rules: RuleSet,
+    cfg: Optional[EngineConfig] = None,
+    as_terms: bool = True,
+    finalize_threads: int = 0,
+) -> BatchResult:
+    """Reduce independent nets in one launch (one CTA per net)."""
+    cfg = cfg if cfg is not None else EngineConfig(collect_stats=False)
+    if not configs:
+        return BatchResult([], 0.0, 0, 0, 0)
+    errs = _errors_for(configs[0])
+    if cfg.slot_count is not None and cfg.slot_count < rules.max_rhs_size:
+        raise getattr(errs, "SlotOverflow", SlotOverflow)(
+            f"slot_count {cfg.slot_count} is smaller than the largest rule rhs ({rules.max_rhs_size})"
+        )
+    ctx = _native.context(getattr(cfg, "device", 0))
+    prep = prepare(configs, rules)
+    with ctx.lock:
+        code, ms = run_prepared(ctx, prep, cfg)
+        if code != _native.OK:
+            for i in range(len(configs)):
+                st = ctx.stats(i)
+                if st.status != _native.OK:
+                    _raise_status(st.status, st, prep.labels, cfg, errs)
+        ti, tc, mr, _nf = ctx.totals()
+        stats = [ctx.stats(i) for i in range(len(configs))]
+        finals = [None] * len(configs)
+        rows = [None] * len(configs)
+        if as_terms:
+            ctx.finalize(0xFFFFFFFF, finalize_threads)
+            for i in range(len(configs)):
+                finals[i] = ctx.result(i)
+        if cfg.collect_stats:
+            rows = [ctx.rounds(i) for i in range(len(configs))]
+    out = []
+    LS = _loop_stats_class(configs[0])
+    ER = _result_class(configs[0])
+    for i, c in enumerate(configs):
+        final = None
+        if finals[i] is not None:
+            final = unflatten(*finals[i], prep.labels, prep.flats[i], term_classes(c))
+        loops = []
+        if rows[i] is not None:
+            loops = [LS(j + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for j, r in enumerate(rows[i])]
+        out.append(ER(final, loops, int(stats[i].interactions), int(stats[i].communications)))
+    return BatchResult(out, ms, ti, tc, mr)
+
+
+def evaluate_sharded(
+    configs: Sequence[Configuration],
+    rules: RuleSet,
+    devices: Sequence[int],
+    cfg: Optional[EngineConfig] = None,
+    as_terms: bool = True,
+) -> BatchResult:
+    """Split a batch into contiguous shards, one per device, reduced concurrently.
+
+    ctypes releases the GIL for every C call, so one host thread per device
+    keeps all GPUs busy. Results are gathered in input order.
+    """
+    devices = list(devices)
+    n = len(configs)
+    if not devices:
+        raise ValueError("no devices")
+    bounds = [n * k // len(devices) for k in range(len(devices) + 1)]
+    parts: list = [None] * len(devices)
+    errors: list = []
+
+    def work(k: int) -> None:
+        try:
+            import dataclasses
+
+            base = cfg if cfg is not None else EngineConfig(collect_stats=False)
+            c = dataclasses.replace(base, device=devices[k])
+            parts[k] = evaluate_batch(configs[bounds[k] : bounds[k + 1]], rules, c, as_terms)
+        except BaseException as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(devices)) if bounds[k] < bounds[k + 1]]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    done = [p for p in parts if p is not None]
+    return BatchResult(
+        results=[r for p in done for r in p.results],
+        device_ms=max(p.device_ms for p in done),
+        total_interactions=sum(p.total_interactions for p in done),
+        total_communications=sum(p.total_communications for p in done),
+        max_rounds=max(p.max_rounds for p in done),
+    )
+
+
+def finalize(eqs: Sequence[Equation], interface: Sequence[Term]) -> Configuration:
+    """Sequential cleanup (engine.py:287-362) via the native host routine."""
+    from .core import Var as _V
+
+    probe = next(iter(list(interface) + [e.lhs for e in eqs]), None)
+    cfg = Configuration(tuple(interface), tuple(eqs))
+    classes = term_classes(cfg)
+    if probe is not None:
+        mod = importlib.import_module(type(probe).__module__)
+        if all(hasattr(mod, n) for n in ("Var", "Agent", "Equation", "Configuration")):
+            classes = (mod.Var, mod.Agent, mod.Equation, mod.Configuration)
+    labels = Labels()
+    flat = flatten(cfg, labels)
+    agents, iface, feqs, alive = _native.finalize_flat(
+        flat.agents.copy(), flat.iface.copy(), flat.eqs.copy(), len(flat.var_ids)
+    )
+    Var, Agent, Equation_, Configuration_ = classes
+    syms = labels.symbols
+    vmap = flat.var_ids
+
+    def build(r: int):
+        # iterative post-order over the mutated arena
+        if r & 0x80000000:
+            return Var(vmap[r & 0x7FFFFFFF])
+        out: dict[int, object] = {}
+        work = [(r, False)]
+        while work:
+            a, done = work.pop()
+            if a in out:
+                continue
+            lab = int(agents[a, 0])
+            ports = [int(p) for p in agents[a, 1 : 1 + syms[lab].arity]]
+            if done:
+                kids = tuple(Var(vmap[p & 0x7FFFFFFF]) if p & 0x80000000 else out[p] for p in ports)
+                out[a] = Agent(syms[lab], kids)
+            else:
+                work.append((a, True))
+                for p in ports:
+                    if not p & 0x80000000:
+                        work.append((p, False))
+        return out[r]
+
+    _ = _V
+    return Configuration_(
+        tuple(build(int(r)) for r in iface),
+        tuple(Equation_(build(int(l)), build(int(rr))) for (l, rr), ok in zip(feqs.reshape(-1, 2), alive) if ok),
+    )

@@ -1,0 +1,248 @@
+"""Host <-> device formats: rule-table compiler and net flattener.
+
+``compile_rules`` turns a ``RuleSet`` (the reference's Rule/RuleSet,
+core.py:158-251, or this package's mirror) into the rule blob documented in
+include/inet_b200.h: a dense ``[label][label] -> (rule, swap)`` table plus one
+16-word record per rule listing its new agents and right-hand-side equations
+as *sources* (port k of either pattern agent, fresh variable j, new agent m).
+This is ``find_rule`` + ``instantiate`` (core.py:281-312) compiled once.
+
+``flatten`` turns a ``Configuration`` into agent records / equation refs /
+interface refs with variables renumbered densely; ``unflatten`` rebuilds
+terms of the caller's own classes from a device normal form, mapping input
+variables back to their ids and numbering fresh ones from
+``config.max_var_id() + 1`` like the reference's allocator (engine.py:196).
+"""
+
+from __future__ import annotations
+
+import sys
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .core import is_var
+from .errors import UnsupportedNet
+
+NONE = 0xFFFFFFFF
+VAR = 0x80000000
+MAGIC = 0x31524E49
+MAX_ARITY, MAX_LABELS, MAX_RULES = 3, 64, 256
+MAX_NEW, MAX_EQ, MAX_FRESH = 8, 8, 8
+SRC_FRESH, SRC_NEW, SRC_NONE = 6, 14, 22
+
+
+@dataclass
+class Labels:
+    """Label numbering shared by a rule blob and the nets reduced with it."""
+
+    symbols: list = field(default_factory=list)  # label -> Symbol object
+    index: dict = field(default_factory=dict)  # name -> label
+
+    def add(self, sym) -> int:
+        lab = self.index.get(sym.name)
+        if lab is not None:
+            if self.symbols[lab].arity != sym.arity:
+                raise UnsupportedNet(f"symbol {sym.name} used with two arities")
+            return lab
+        if sym.arity > MAX_ARITY:
+            raise UnsupportedNet(f"{sym.name} has arity {sym.arity} > {MAX_ARITY}")
+        if len(self.symbols) >= MAX_LABELS:
+            raise UnsupportedNet(f"more than {MAX_LABELS} agent symbols")
+        self.index[sym.name] = len(self.symbols)
+        self.symbols.append(sym)
+        return self.index[sym.name]
+
+    @classmethod
+    def of(cls, rules, configs=()) -> "Labels":
+        lab = cls()
+        for s in rules.symbols.values():
+            lab.add(s)
+        for cfg in configs:
+            for t in _roots(cfg):
+                work = [t]
+                while work:
+                    x = work.pop()
+                    if not is_var(x):
+                        if x.sym.name not in lab.index:
+                            lab.add(x.sym)
+                        work.extend(x.children)
+        return lab
+
+
+def _roots(cfg):
+    yield from cfg.interface
+    for e in cfg.equations:
+        yield e.lhs
+        yield e.rhs
+
+
+def compile_rules(rules, labels: Labels) -> np.ndarray:
+    """RuleSet -> uint32 rule blob (layout in include/inet_b200.h)."""
+    L = len(labels.symbols)
+    rule_list = list(rules.rules.values())
+    if len(rule_list) > MAX_RULES:
+        raise UnsupportedNet(f"more than {MAX_RULES} rules")
+    pair = np.full(L * L + (L * L) % 2, 0xFFFF, dtype=np.uint16)
+    recs = np.zeros((len(rule_list), 16), dtype=np.uint32)
+    for ri, rule in enumerate(rule_list):
+        la = labels.index[rule.lhs_a.name]
+        lb = labels.index[rule.lhs_b.name]
+        pair[la * L + lb] = ri << 1
+        if la != lb:
+            pair[lb * L + la] = (ri << 1) | 1
+        env = {}
+        for k, v in enumerate(rule.a_vars):
+            env[v] = k
+        for k, v in enumerate(rule.b_vars):
+            env[v] = 3 + k
+        if len(rule.bound_vars) > MAX_FRESH:
+            raise UnsupportedNet(f"rule {rule.lhs_a.name}><{rule.lhs_b.name}: too many fresh variables")
+        for j, v in enumerate(rule.bound_vars):
+            env[v] = SRC_FRESH + j
+        new_agents: list[list[int]] = []  # [label, src0, src1, src2]
+
+        def source(term) -> int:
+            if is_var(term):
+                return env[term.id]
+            # allocate parent before children so reused slots go to outer agents
+            slot = len(new_agents)
+            if slot >= MAX_NEW:
+                raise UnsupportedNet(f"rule {rule.lhs_a.name}><{rule.lhs_b.name}: too many rhs agents")
+            rec = [labels.index[term.sym.name], SRC_NONE, SRC_NONE, SRC_NONE]
+            new_agents.append(rec)
+            work = [(term, rec)]
+            while work:
+                t, r = work.pop()
+                for k, ch in enumerate(t.children):
+                    if is_var(ch):
+                        r[1 + k] = env[ch.id]
+                    else:
+                        s = len(new_agents)
+                        if s >= MAX_NEW:
+                            raise UnsupportedNet(
+                                f"rule {rule.lhs_a.name}><{rule.lhs_b.name}: too many rhs agents")
+                        cr = [labels.index[ch.sym.name], SRC_NONE, SRC_NONE, SRC_NONE]
+                        new_agents.append(cr)
+                        r[1 + k] = SRC_NEW + s
+                        work.append((ch, cr))
+            return SRC_NEW + slot
+
+        if len(rule.rhs) > MAX_EQ:
+            raise UnsupportedNet(f"rule {rule.lhs_a.name}><{rule.lhs_b.name}: rhs has > {MAX_EQ} equations")
+        eq_src = [(source(e.lhs), source(e.rhs)) for e in rule.rhs]
+        recs[ri, 0] = len(new_agents) | (len(eq_src) << 8) | (len(rule.bound_vars) << 16)
+        for m, (lab, s0, s1, s2) in enumerate(new_agents):
+            recs[ri, 1 + m] = lab | (s0 << 8) | (s1 << 16) | (s2 << 24)
+        for e, (sl, sr) in enumerate(eq_src):
+            recs[ri, 9 + e // 2] |= (sl | (sr << 8)) << (16 * (e & 1))
+    head = np.array([MAGIC, L, len(rule_list), 0], dtype=np.uint32)
+    return np.concatenate([head, pair.view(np.uint32), recs.reshape(-1)]).astype(np.uint32)
+
+
+@dataclass
+class FlatNet:
+    agents: np.ndarray  # (n, 4) uint32
+    eqs: np.ndarray  # (m, 2) uint32
+    iface: np.ndarray  # (k,) uint32
+    var_ids: list  # dense id -> original id
+    fresh_base: int  # first id for fresh variables on the way back
+
+
+def flatten(config, labels: Labels) -> FlatNet:
+    """Configuration -> flat device input (net-local refs)."""
+    agents: list[tuple] = []
+    dense: dict[int, int] = {}
+    var_ids: list[int] = []
+    index = labels.index
+
+    def ref(term) -> int:
+        if is_var(term):
+            d = dense.get(term.id)
+            if d is None:
+                d = dense[term.id] = len(var_ids)
+                var_ids.append(term.id)
+            return VAR | d
+        # iterative: reserve the record, fill ports afterwards
+        root = len(agents)
+        agents.append(None)
+        work = [(term, root)]
+        while work:
+            t, slot = work.pop()
+            if len(t.children) > MAX_ARITY:
+                raise UnsupportedNet(f"{t.sym.name} has arity {len(t.children)} > {MAX_ARITY}")
+            ports = [NONE, NONE, NONE]
+            for k, ch in enumerate(t.children):
+                if is_var(ch):
+                    d = dense.get(ch.id)
+                    if d is None:
+                        d = dense[ch.id] = len(var_ids)
+                        var_ids.append(ch.id)
+                    ports[k] = VAR | d
+                else:
+                    s = len(agents)
+                    agents.append(None)
+                    ports[k] = s
+                    work.append((ch, s))
+            lab = index.get(t.sym.name)
+            if lab is None:
+                lab = labels.add(t.sym)
+            agents[slot] = (lab, ports[0], ports[1], ports[2])
+        return root
+
+    iface = [ref(t) for t in config.interface]
+    eqs = [(ref(e.lhs), ref(e.rhs)) for e in config.equations]
+    max_id = max(var_ids) if var_ids else -1
+    return FlatNet(
+        agents=np.array(agents, dtype=np.uint32).reshape(-1, 4),
+        eqs=np.array(eqs, dtype=np.uint32).reshape(-1, 2),
+        iface=np.array(iface, dtype=np.uint32),
+        var_ids=var_ids,
+        fresh_base=max_id + 1,
+    )
+
+
+def term_classes(config):
+    """(Var, Agent, Equation, Configuration) classes of the caller's objects."""
+    mod = sys.modules.get(type(config).__module__)
+    if mod is not None and all(hasattr(mod, n) for n in ("Var", "Agent", "Equation", "Configuration")):
+        return mod.Var, mod.Agent, mod.Equation, mod.Configuration
+    from . import core
+
+    return core.Var, core.Agent, core.Equation, core.Configuration
+
+
+def unflatten(agents: np.ndarray, iface: np.ndarray, eqs: np.ndarray, labels: Labels, flat: FlatNet,
+              classes) -> object:
+    """Device normal form (preorder agents) -> Configuration of ``classes``."""
+    Var, Agent, Equation, Configuration = classes
+    n_in = len(flat.var_ids)
+    var_ids = flat.var_ids
+    base = flat.fresh_base
+    vcache: dict[int, object] = {}
+
+    def var(d: int):
+        v = vcache.get(d)
+        if v is None:
+            v = vcache[d] = Var(var_ids[d] if d < n_in else base + (d - n_in))
+        return v
+
+    syms = labels.symbols
+    built: list = [None] * len(agents)
+    rows = agents.tolist()
+    # preorder numbering puts children after parents: build back to front
+    for a in range(len(rows) - 1, -1, -1):
+        lab, p0, p1, p2 = rows[a]
+        sym = syms[lab]
+        kids = []
+        for p in (p0, p1, p2)[: sym.arity]:
+            kids.append(var(p & ~VAR) if p & VAR else built[p])
+        built[a] = Agent(sym, tuple(kids))
+
+    def term(r: int):
+        return var(r & ~VAR) if r & VAR else built[r]
+
+    return Configuration(
+        tuple(term(int(r)) for r in iface),
+        tuple(Equation(term(int(l)), term(int(r))) for l, r in eqs.reshape(-1, 2)),
+    )

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA engine against the reference fixtures and the oracle.
+
+Bar: the canonical printed normal form is byte-identical and
+the total interaction count is identical. The per-round series is the
+device's own (fixpoint linking per round), so only its invariants are checked.
+"""
+
+import hashlib
+import random
+
+import pytest
+
+from golden_io import load, to_config, to_rules
+from oracle import oracle as O
+from paper_1404_0076_b200 import (
+    Agent,
+    Configuration,
+    EngineConfig,
+    Equation,
+    Var,
+    evaluate,
+    evaluate_batch,
+    parse_program,
+    print_configuration,
+)
+from paper_1404_0076_b200 import errors, programs
+
+pytestmark = pytest.mark.gpu
+
+PROGRAMS = load("programs.json")
+CASES = load("cases.json")
+ARITH = load("arith.json")
+
+
+def _sha(text):
+    return hashlib.sha256(text.encode()).hexdigest()
+
+
+def _case_inputs(case):
+    if "program" in case:
+        prog = programs.program(case["program"])
+        return prog.build_input(*case["params"]), prog.rules
+    if "source" in case:
+        sp = parse_program(case["source"])
+        return sp.net, sp.rules
+    return to_config(case["net"]), to_rules(PROGRAMS["arith"])
+
+
+def _check_loops(res):
+    assert res.loops, "collect_stats=True must produce rows"
+    assert sum(s.interactions for s in res.loops) == res.total_interactions
+    assert sum(s.communications for s in res.loops) == res.total_communications
+    assert (res.loops[-1].interactions, res.loops[-1].communications) == (0, 0)
+    assert [s.loop_index for s in res.loops] == list(range(1, len(res.loops) + 1))
+    if len(res.loops) >= 2:
+        assert res.loops[-1].live_equations == res.loops[-2].live_equations
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_reference_fixture(case):
+    config, rules = _case_inputs(case)
+    cfg = EngineConfig(**case.get("engine_config", {}))
+    if "error" in case:
+        with pytest.raises(getattr(errors, case["error"])) as ei:
+            evaluate(config, rules, cfg)
+        if case.get("error_pair"):
+            assert list(ei.value.pair) == case["error_pair"]
+        return
+    res = evaluate(config, rules, cfg)
+    text = print_configuration(res.final)
+    assert res.total_interactions == case["interactions"]
+    assert _sha(text) == case["print_sha256"]
+    _check_loops(res)
+
+
+def test_ackermann_communications_equal_reference():
+    # no var=var equations arise in Ackermann, so the merge count is schedule-free
+    for case in CASES:
+        if case.get("program") == "ackermann":
+            config, rules = _case_inputs(case)
+            assert evaluate(config, rules).total_communications == case["communications"], case["name"]
+
+
+def test_arith_551_nets_one_launch():
+    rules = to_rules(PROGRAMS["arith"])
+    configs = [to_config(c["net"]) for c in ARITH]
+    out = evaluate_batch(configs, rules, EngineConfig(collect_stats=False))
+    for case, res in zip(ARITH, out.results):
+        assert res.total_interactions == case["interactions"], case["name"]
+        assert _sha(print_configuration(res.final)) == case["print_sha256"], case["name"]
+
+
+def test_arith_nets_single_launch_each():
+    rules = to_rules(PROGRAMS["arith"])
+    for case in ARITH[:60]:
+        res = evaluate(to_config(case["net"]), rules)
+        assert res.total_interactions == case["interactions"], case["name"]
+        assert _sha(print_configuration(res.final)) == case["print_sha256"], case["name"]
+        _check_loops(res)
+
+
+def _random_arith_net(rng, syms, budget):
+    """Own generator (not the reference's netgen): nested Add/Dup/Eps over literals."""
+    eqs, nxt = [], [0]
+
+    def fresh():
+        nxt[0] += 1
+        return Var(nxt[0] - 1)
+
+    def lit():
+        return programs.build_nat(rng.randint(0, 4))
+
+    def expr(b):
+        roll = rng.random()
+        if b <= 2 or roll < 0.3:
+            return lit()
+        if roll < 0.6:
+            r = fresh()
+            eqs.append(Equation(Agent(syms["Add"], (r, expr(b // 2))), expr(b // 2)))
+            return r
+        if roll < 0.85:
+            a, c, r = fresh(), fresh(), fresh()
+            eqs.append(Equation(Agent(syms["Dup"], (a, c)), expr(b - 2)))
+            eqs.append(Equation(Agent(syms["Add"], (r, a)), c))
+            return r
+        eqs.append(Equation(Agent(syms["Eps"]), expr(b // 3)))
+        return expr(b // 2)
+
+    top = expr(budget)
+    return Configuration((top,), tuple(eqs))
+
+
+def test_random_arith_nets_against_oracle():
+    rules = programs.load_rules("arith")
+    orules = O.rules_for("arith")
+    rng = random.Random(1234)
+    nets = [_random_arith_net(rng, rules.symbols, rng.choice([8, 40, 200, 1000])) for _ in range(300)]
+    out = evaluate_batch(nets, rules, EngineConfig(collect_stats=False))
+    for net, res in zip(nets, out.results):
+        want = O.run_config(net, orules, collect=False)
+        assert res.total_interactions == want.interactions
+        assert print_configuration(res.final) == want.printed()
+
+
+@pytest.mark.parametrize("params,interactions,sha", [
+    ((3, 8), 5_574_030, "b85606c71178de4b"),
+    ((3, 10), 89_404_824, "981fd9bfe283f466"),
+])
+def test_large_ackermann(params, interactions, sha):
+    prog = programs.program("ackermann")
+    res = evaluate(prog.build_input(*params), prog.rules)
+    assert res.total_interactions == interactions
+    text = print_configuration(res.final)
+    assert _sha(text).startswith(sha)
+    assert programs.nat_value(res.final.interface[0]) == programs.ackermann_value(*params)
+    _check_loops(res)
+
+
+def test_batch_of_ackermann_3_6():
+    prog = programs.program("ackermann")
+    nets = [prog.build_input(3, 6) for _ in range(512)]
+    out = evaluate_batch(nets, prog.rules, EngineConfig(collect_stats=False), as_terms=True)
+    assert out.total_interactions == 512 * 344_964
+    for r in out.results:
+        assert r.total_interactions == 344_964
+        assert programs.nat_value(r.final.interface[0]) == 509
+
+
+def test_mixed_batch_against_oracle():
+    prog = programs.program("ackermann")
+    orules = O.rules_for("ackermann")
+    rng = random.Random(7)
+    params = [(rng.randint(0, 3), rng.randint(0, 6)) for _ in range(200)]
+    nets = [prog.build_input(m, n) for m, n in params]
+    out = evaluate_batch(nets, prog.rules, EngineConfig(collect_stats=False))
+    for (m, n), net, res in zip(params, nets, out.results):
+        want = O.run_config(net, orules, collect=False)
+        assert res.total_interactions == want.interactions, (m, n)
+        assert print_configuration(res.final) == want.printed(), (m, n)
+
+
+def test_errors_map_to_reference_classes():
+    rules = programs.load_rules("addition")
+    sp = parse_program("Add(r,y) >< S(x) => Add(w,y)=x, r=S(w);\nAdd(r,y) >< Z => r=y;\nnet r : Add(r, Z) = S(Z);")
+    with pytest.raises(errors.SlotOverflow):
+        evaluate(sp.net, sp.rules, EngineConfig(slot_count=1))
+    loop = parse_program("Loop >< Z => Loop = Z;\nnet : Loop = Z;")
+    with pytest.raises(errors.LoopCapExceeded) as ei:
+        evaluate(loop.net, loop.rules, EngineConfig(max_loops=5))
+    assert ei.value.max_loops == 5
+    bad = parse_program("A >< B => ;\nnet : A = C;")
+    with pytest.raises(errors.NoRuleForPair) as ei:
+        evaluate(bad.net, bad.rules)
+    assert ei.value.pair == ("A", "C")
+    del rules
+
+
+def test_collect_stats_off_and_arena_growth():
+    prog = programs.program("fibonacci")
+    res = evaluate(prog.build_input(15), prog.rules, EngineConfig(collect_stats=False))
+    assert res.loops == [] and res.total_interactions == 11_092
+    # a tiny initial arena must grow transparently
+    from paper_1404_0076_b200 import _native, engine
+
+    prep = engine.prepare([prog.build_input(18)], prog.rules)
+    ctx = _native.context(0)
+    with ctx.lock:
+        ctx.load_rules(prep.blob)
+        ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
+        k = engine.native_cfg(EngineConfig(collect_stats=False))
+        k.cap_agents, k.cap_vars = 128, 128
+        code, _ = ctx.reduce(k)
+        st = ctx.stats(0)
+        ctx._blob_key = None
+    assert code == _native.OK
+    assert st.interactions == 50_515 and st.cap_agents > 128
