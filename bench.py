@@ -352,7 +352,9 @@ def run_ours(args) -> None:
             "data": "synthetic (deterministic Ackermann nets built by paper_1404_0076_b200.programs, no RNG)",
             "config": dict(wl, parallelism=f"dp{world} (nets sharded, no collective)",
                            interactions_per_net=per_net, rounds_per_net=max_rounds,
-                           threads_per_net=engine.native_cfg(ecfg).threads or "auto"),
+                           threads_per_net=engine.native_cfg(ecfg).threads or "auto",
+                           tier="SMG"[ctx.stats(0).tier], agent_hw=ctx.stats(0).agent_hw,
+                           var_hw=ctx.stats(0).var_hw),
             "e2e": {"value": e2e_value, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "path": "C ABI inet_batch_load+inet_batch_reduce+inet_batch_finalize, host flat buffers"},
@@ -386,7 +388,8 @@ def run_ours(args) -> None:
                 flush_l2()
                 best.append(c2.rerun(kk))
             ms = min(best)
-            singles[label] = {"interactions": golden, "rounds": st.rounds, "device_ms": ms,
+            singles[label] = {"interactions": golden, "rounds": st.rounds, "device_ms": ms, "tier": "SMG"[st.tier],
+                              "agent_hw": st.agent_hw, "var_hw": st.var_hw,
                               "interactions_per_s": golden / (ms / 1000.0),
                               "us_per_round": 1000.0 * ms / max(st.rounds, 1)}
             c2.close()

@@ -99,7 +99,7 @@ typedef struct inet_net_stats {
   uint32_t n_residual;     /* parked equations at the fixpoint (input of finalize) */
   uint32_t cap_agents;     /* capacities the successful run used */
   uint32_t cap_vars;
-  uint32_t reserved;
+  uint32_t tier;           /* residency tier used: 0 S (shared), 1 M (mixed), 2 G (global) */
 } inet_net_stats;
 
 /* Context: one device, one stream, device buffers reused across calls. */

@@ -65,7 +65,7 @@ class NetStats(C.Structure):
         ("n_residual", C.c_uint32),
         ("cap_agents", C.c_uint32),
         ("cap_vars", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("tier", C.c_uint32),
     ]
 
 

@@ -17,11 +17,29 @@
 // the merged equation (reduce_by_key's merge lambda, engine.py:161-165).
 // var=var equations are keyed by the smaller id as in engine.py:150-153.
 //
+// Because a net never leaves its CTA, every counter (queue tail, allocators,
+// statistics) and both free rings live in shared memory. Three residency
+// tiers share this code (chosen per launch by the host, falling back S -> G
+// or M -> G when a net outgrows its shared-memory arena):
+//
+//   S  agents, variable slots, queues in shared memory (small nets: the
+//      4096 x A(3,6) batch, several CTAs per SM);
+//   M  variable slots and queues in shared memory, agents in global memory
+//      (one large net per SM, e.g. A(3,10)); the exchanges that link
+//      variables are shared-memory atomics, the only L2 round trip per
+//      interaction is the read of the two agents;
+//   G  everything but the counters and rings in global memory (unbounded).
+//
+// Tiers S and M pack an active pair into one 32-bit queue word (two 16-bit
+// agent indices) and keep 16-bit free rings, so their arenas are capped at
+// 65,535 agents.
+//
 // Memory: agents are 16-byte records {label, port0..2}. The two agents of an
 // active pair are dead after the rewrite; their slots are reused in place for
 // the first two right-hand-side agents, others come from a round-phased free
-// ring, then from a bump pointer. Variable ids are recycled the same way once
-// both occurrences have met.
+// ring (ids freed in round r become allocatable in round r+1), then from a
+// bump pointer. Variable ids are recycled the same way once both occurrences
+// have met. A full ring drops the id (it is simply never reused).
 #pragma once
 #include <cstdint>
 
@@ -36,24 +54,68 @@ constexpr int kEnvNew = 14;
 constexpr int kEnvNone = 22;
 constexpr int kEnvSize = 24;
 constexpr int kRuleWords = 16;
+constexpr int kFastEq = 4;  // rhs equations linked with overlapped exchanges
 
-// Counters of one round; three rotate so that round r writes ctr[r%3] while
-// every thread reads the finished ctr[(r-1)%3] and thread 0 clears ctr[(r+1)%3].
+enum : int { kTierS = 0, kTierM = 1, kTierG = 2 };
+
+template <int kTier>
+struct Traits {
+  using Ring = uint16_t;
+  static constexpr bool kAgentsSmem = kTier == kTierS;
+  static constexpr bool kSlotsSmem = true;
+  static constexpr bool kPacked = true;
+};
+template <>
+struct Traits<kTierG> {
+  using Ring = uint32_t;
+  static constexpr bool kAgentsSmem = false;
+  static constexpr bool kSlotsSmem = false;
+  static constexpr bool kPacked = false;
+};
+
+// Counters of the running round, bumped by every thread while it works.
 struct RoundCtr {
   uint32_t qcount;  // active pairs queued for the next round
   uint32_t atake;   // agent ring entries taken
-  uint32_t afree;   // agents freed into the ring
+  uint32_t afree;   // agents offered to the ring
   uint32_t vtake;
   uint32_t vfree;
   uint32_t ints;
   uint32_t comms;
   int32_t parked;   // delta of parked equations
-  uint32_t err;     // any failure in this round (read by all threads next round)
-  uint32_t pad[7];
+  uint32_t err;     // any failure in this round
+  uint32_t pad[3];
 };
 
+// Parameters of the next round, written by the last warp to finish a round
+// (before the round's barrier) and read by every thread after it.
+struct Header {
+  uint32_t n;       // active pairs in the queue
+  uint32_t stop;    // leave the loop
+  uint32_t lo_a, hi_a, lo_v, hi_v;  // ring windows allocatable in this round
+  uint32_t pad[2];
+};
+
+// Shared-memory control block of the net a CTA is reducing.
+struct Ctl {
+  RoundCtr ctr;
+  Header hdr;
+  uint32_t done_warps;
+  uint32_t agent_bump;
+  uint32_t var_bump;
+  uint32_t err_code;
+  uint32_t err_a;
+  uint32_t err_b;
+  uint32_t rounds;
+  int32_t parked_total;
+  unsigned long long t_prev;
+  unsigned long long tot_i;
+  unsigned long long tot_c;
+  uint32_t scratch[34];
+};
+
+// Global result block of one net (read by the host).
 struct NetCtl {
-  RoundCtr ctr[3];
   uint32_t agent_bump;
   uint32_t var_bump;
   uint32_t err;
@@ -67,23 +129,31 @@ struct NetCtl {
   uint32_t pad[4];
 };
 
-// Per-net device view; all arrays are private to the net.
+// Per-net device view of its private global arrays.
 struct NetDesc {
-  uint4* agents;       // cap_agents
-  uint32_t* vslot;     // cap_vars, kNone = no parked side
-  uint32_t* aring;     // amask+1 >= cap_agents
-  uint32_t* vring;     // vmask+1 >= cap_vars
-  uint2* queue;        // 2 * cap_queue (double buffer)
+  uint4* agents;       // cap_agents (tiers M/G arena; tier S result copy)
+  uint32_t* vslot;     // cap_vars (tier G)
+  uint2* queue;        // 2 * cap_queue (tier G)
   uint4* stats;        // cap_rounds rows {ints, comms, live, ns} or null
   uint2* residual;     // cap_vars
   NetCtl* ctl;
-  uint32_t* rule_hist;  // interactions per rule (accounting runs) or null
+  uint32_t* rule_hist; // interactions per rule (accounting runs) or null
   uint32_t cap_agents, cap_vars, cap_queue, cap_rounds;
-  uint32_t amask, vmask;
   // initial contents (device copies of the caller's flat arrays)
   const uint4* in_agents;
   const uint2* in_eqs;
   uint32_t n_in_agents, n_in_eqs, n_in_vars, pad;
+};
+
+// Launch-wide shape: ring sizes and the shared-memory capacities.
+struct Shape {
+  uint32_t ring_a, ring_v;        // powers of two
+  uint32_t res_agents;            // tier S agents in shared memory
+  uint32_t res_vars;              // tiers S/M variable slots in shared memory
+  uint32_t res_queue;             // tiers S/M queue words per buffer
+  uint32_t max_rounds;
+  uint32_t rule_words;            // pair table + rule records (words)
+  uint32_t n_labels;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -92,44 +162,56 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-__device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
+template <class T>
+__device__ __forceinline__ T vload(const T* p) {
+  return *reinterpret_cast<const volatile T*>(p);
+}
 
 // Thread-private view of the running round.
+template <int kTier>
 struct Round {
+  using Ring = typename Traits<kTier>::Ring;
   const NetDesc* d;
+  Ctl* ctl;
   uint4* agents;
   uint32_t* vslot;
+  Ring* aring;
+  Ring* vring;
+  void* out;
   RoundCtr* cur;
-  uint2* out;
   const uint16_t* pair;
   const uint32_t* rules;
   uint32_t n_labels;
+  uint32_t cap_agents, cap_vars, cap_queue;
+  uint32_t amask, vmask;
   uint32_t lo_a, hi_a, lo_v, hi_v;  // ring windows available this round
   uint32_t ints, comms;
   int32_t parked;
   bool failed;
 };
 
-__device__ __forceinline__ void fail(Round& c, uint32_t code, uint32_t a = 0, uint32_t b = 0) {
+template <int kTier>
+__device__ __forceinline__ void fail(Round<kTier>& c, uint32_t code, uint32_t a = 0, uint32_t b = 0) {
   c.failed = true;
   c.cur->err = 1u;
-  if (atomicCAS(&c.d->ctl->err, 0u, code) == 0u) {
-    c.d->ctl->err_a = a;
-    c.d->ctl->err_b = b;
+  if (atomicCAS(&c.ctl->err_code, 0u, code) == 0u) {
+    c.ctl->err_a = a;
+    c.ctl->err_b = b;
   }
 }
 
-__device__ __forceinline__ bool alloc_vars(Round& c, uint32_t nf, uint32_t* out) {
+template <int kTier>
+__device__ __forceinline__ bool alloc_vars(Round<kTier>& c, uint32_t nf, uint32_t* out) {
   if (nf == 0) return true;
   const uint32_t t = atomicAdd(&c.cur->vtake, nf);
   const uint32_t avail = c.hi_v - c.lo_v;
   uint32_t got = 0;
   if (t < avail) got = min(avail - t, nf);
-  for (uint32_t j = 0; j < got; ++j) out[j] = kVar | c.d->vring[(c.lo_v + t + j) & c.d->vmask];
+  for (uint32_t j = 0; j < got; ++j) out[j] = kVar | c.vring[(c.lo_v + t + j) & c.vmask];
   if (got < nf) {
     const uint32_t need = nf - got;
-    const uint32_t b = atomicAdd(&c.d->ctl->var_bump, need);
-    if (b + need > c.d->cap_vars) {
+    const uint32_t b = atomicAdd(&c.ctl->var_bump, need);
+    if (b + need > c.cap_vars) {
       fail(c, INET_ERR_ARENA, 1);
       return false;
     }
@@ -138,16 +220,17 @@ __device__ __forceinline__ bool alloc_vars(Round& c, uint32_t nf, uint32_t* out)
   return true;
 }
 
-__device__ __forceinline__ bool alloc_agents(Round& c, uint32_t n, uint32_t* out) {
+template <int kTier>
+__device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, uint32_t* out) {
   const uint32_t t = atomicAdd(&c.cur->atake, n);
   const uint32_t avail = c.hi_a - c.lo_a;
   uint32_t got = 0;
   if (t < avail) got = min(avail - t, n);
-  for (uint32_t j = 0; j < got; ++j) out[j] = c.d->aring[(c.lo_a + t + j) & c.d->amask];
+  for (uint32_t j = 0; j < got; ++j) out[j] = c.aring[(c.lo_a + t + j) & c.amask];
   if (got < n) {
     const uint32_t need = n - got;
-    const uint32_t b = atomicAdd(&c.d->ctl->agent_bump, need);
-    if (b + need > c.d->cap_agents) {
+    const uint32_t b = atomicAdd(&c.ctl->agent_bump, need);
+    if (b + need > c.cap_agents) {
       fail(c, INET_ERR_ARENA, 0);
       return false;
     }
@@ -156,63 +239,88 @@ __device__ __forceinline__ bool alloc_agents(Round& c, uint32_t n, uint32_t* out
   return true;
 }
 
-__device__ __forceinline__ void free_agent(Round& c, uint32_t a) {
+template <int kTier>
+__device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
   const uint32_t f = atomicAdd(&c.cur->afree, 1u);
-  c.d->aring[(c.hi_a + f) & c.d->amask] = a;
+  const uint32_t pos = c.hi_a + f;
+  if (pos - c.lo_a <= c.amask) c.aring[pos & c.amask] = a;  // else dropped
 }
 
-__device__ __forceinline__ void free_var(Round& c, uint32_t x) {
+template <int kTier>
+__device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
   const uint32_t f = atomicAdd(&c.cur->vfree, 1u);
-  c.d->vring[(c.hi_v + f) & c.d->vmask] = x;
+  const uint32_t pos = c.hi_v + f;
+  if (pos - c.lo_v <= c.vmask) c.vring[pos & c.vmask] = x;
 }
 
-__device__ __forceinline__ void push_active(Round& c, uint32_t l, uint32_t r) {
+template <int kTier>
+__device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_t r) {
   const uint32_t p = atomicAdd(&c.cur->qcount, 1u);
-  if (p >= c.d->cap_queue) {
+  if (p >= c.cap_queue) {
     fail(c, INET_ERR_ARENA, 2);
     return;
   }
-  c.out[p] = make_uint2(l, r);
+  if constexpr (Traits<kTier>::kPacked)
+    static_cast<uint32_t*>(c.out)[p] = (l << 16) | r;  // both < 65536 in tiers S/M
+  else
+    static_cast<uint2*>(c.out)[p] = make_uint2(l, r);
 }
 
-// Link one equation: park it on its variable or merge with the parked
-// partner, repeating on the merged equation until it is active or parked.
-__device__ __forceinline__ void link(Round& c, uint32_t l, uint32_t r) {
+// Key and parked value of a non-active equation: var=var keys on the smaller id.
+__device__ __forceinline__ void key_of(uint32_t l, uint32_t r, uint32_t& key, uint32_t& val) {
+  const bool lv = (l & kVar) != 0, rv = (r & kVar) != 0;
+  if (lv && rv) {
+    key = l < r ? l : r;
+    val = l < r ? r : l;
+  } else if (lv) {
+    key = l;
+    val = r;
+  } else {
+    key = r;
+    val = l;
+  }
+}
+
+// Finish an exchange on slot x that returned `old`; continue linking the
+// merged equation {x = old, x = val} -> old = val until it parks or is active.
+template <int kTier>
+__device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old, uint32_t val) {
   while (true) {
-    const bool lv = (l & kVar) != 0, rv = (r & kVar) != 0;
-    if (!lv && !rv) {
-      push_active(c, l, r);
-      return;
-    }
-    uint32_t key, val;
-    if (lv && rv) {
-      key = l < r ? l : r;  // smaller id is the key (engine.py:150-153)
-      val = l < r ? r : l;
-    } else if (lv) {
-      key = l;
-      val = r;
-    } else {
-      key = r;
-      val = l;
-    }
-    const uint32_t x = key & ~kVar;
-    const uint32_t old = atomicExch(&c.vslot[x], val);
     if (old == kNone) {
       c.parked += 1;
       return;
     }
-    // second occurrence: {x = old, x = val} -> old = val; x is dead
-    c.vslot[x] = kNone;
+    c.vslot[x] = kNone;  // x is dead: both occurrences met
     c.comms += 1;
     c.parked -= 1;
     free_var(c, x);
-    l = old;
-    r = val;
+    const uint32_t l = old, r = val;
+    if (((l | r) & kVar) == 0) {
+      push_active(c, l, r);
+      return;
+    }
+    uint32_t key;
+    key_of(l, r, key, val);
+    x = key & ~kVar;
+    old = atomicExch(&c.vslot[x], val);
   }
 }
 
+template <int kTier>
+__device__ __forceinline__ void link(Round<kTier>& c, uint32_t l, uint32_t r) {
+  if (((l | r) & kVar) == 0) {
+    push_active(c, l, r);
+    return;
+  }
+  uint32_t key, val;
+  key_of(l, r, key, val);
+  const uint32_t x = key & ~kVar;
+  settle(c, x, atomicExch(&c.vslot[x], val), val);
+}
+
 // Rewrite one active pair (find_rule + instantiate, core.py:281-312).
-__device__ __forceinline__ void interact(Round& c, uint32_t l, uint32_t r) {
+template <int kTier>
+__device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r) {
   uint4 A = c.agents[l];
   uint4 B = c.agents[r];
   const uint32_t t = c.pair[A.x * c.n_labels + B.x];
@@ -251,26 +359,33 @@ __device__ __forceinline__ void interact(Round& c, uint32_t l, uint32_t r) {
   }
   if (nn < 2) free_agent(c, r);
   if (nn < 1) free_agent(c, l);
-  for (uint32_t e = 0; e < ne; ++e) {
-    const uint32_t h = (R[9 + (e >> 1)] >> ((e & 1u) * 16u)) & 0xFFFFu;
+  // Link the rhs: issue the first exchange of every equation back to back so
+  // their latencies overlap, then settle each.
+  uint32_t xs[kFastEq], olds[kFastEq], vals[kFastEq];
+#pragma unroll
+  for (int e = 0; e < kFastEq; ++e) {
+    xs[e] = kNone;
+    if (e < static_cast<int>(ne)) {
+      const uint32_t h = (R[9 + (e >> 1)] >> ((e & 1) * 16)) & 0xFFFFu;
+      const uint32_t el = env[h & 0xFFu], er = env[h >> 8];
+      if (((el | er) & kVar) == 0) {
+        push_active(c, el, er);
+      } else {
+        uint32_t key;
+        key_of(el, er, key, vals[e]);
+        xs[e] = key & ~kVar;
+        olds[e] = atomicExch(&c.vslot[xs[e]], vals[e]);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < kFastEq; ++e)
+    if (xs[e] != kNone) settle(c, xs[e], olds[e], vals[e]);
+  for (uint32_t e = kFastEq; e < ne; ++e) {
+    const uint32_t h = (R[9 + (e >> 1)] >> ((e & 1) * 16)) & 0xFFFFu;
     link(c, env[h & 0xFFu], env[h >> 8]);
   }
   c.ints += 1;
-}
-
-// Copy a net's input into its private arrays and reset its counters.
-__device__ void init_net(const NetDesc& d) {
-  for (uint32_t i = threadIdx.x; i < d.cap_vars; i += blockDim.x) d.vslot[i] = kNone;
-  for (uint32_t i = threadIdx.x; i < d.n_in_agents; i += blockDim.x) d.agents[i] = d.in_agents[i];
-  for (uint32_t i = threadIdx.x; i < d.n_in_eqs; i += blockDim.x) d.queue[i] = d.in_eqs[i];
-  uint32_t* ctl = reinterpret_cast<uint32_t*>(d.ctl);
-  for (uint32_t i = threadIdx.x; i < sizeof(NetCtl) / 4; i += blockDim.x) ctl[i] = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    d.ctl->ctr[0].qcount = d.n_in_eqs;
-    d.ctl->agent_bump = d.n_in_agents;
-    d.ctl->var_bump = d.n_in_vars;
-  }
 }
 
 // Block-wide exclusive prefix of a 0/1 flag; returns the total.
@@ -297,104 +412,226 @@ __device__ __forceinline__ uint32_t block_scan_flag(bool flag, uint32_t* warp_to
   return total;
 }
 
+// Shared-memory plan (32-bit words):
+//   rule table | Ctl | agent ring | var ring | [S: agents] | [S,M: slots] | [S,M: 2 queues]
+struct SmemPlan {
+  uint32_t ctl_off, aring_off, vring_off, agents_off, slots_off, queue_off, words;
+};
+
+__host__ __device__ inline uint32_t align4(uint32_t w) { return (w + 3u) & ~3u; }
+
+__host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
+  const uint32_t ring_bytes = tier == kTierG ? 4u : 2u;
+  SmemPlan p;
+  p.ctl_off = align4(sh.rule_words);
+  p.aring_off = p.ctl_off + align4(sizeof(Ctl) / 4);
+  p.vring_off = p.aring_off + align4((sh.ring_a * ring_bytes + 3) / 4);
+  p.agents_off = p.vring_off + align4((sh.ring_v * ring_bytes + 3) / 4);
+  p.slots_off = p.agents_off + (tier == kTierS ? 4 * sh.res_agents : 0);
+  p.queue_off = p.slots_off + (tier != kTierG ? align4(sh.res_vars) : 0);
+  p.words = p.queue_off + (tier != kTierG ? align4(2 * sh.res_queue) : 0);
+  return p;
+}
+
 // Reduce one net to its fixpoint; the whole CTA cooperates.
-__device__ void run_net(const NetDesc& d, const uint16_t* pair, const uint32_t* rules, uint32_t n_labels,
-                        uint32_t max_rounds, uint32_t* scratch) {
-  init_net(d);
-  __syncthreads();
-  NetCtl* ctl = d.ctl;
-  Round c;
+template <int kTier>
+__device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair, const uint32_t* rules,
+                        uint32_t* smem) {
+  using T = Traits<kTier>;
+  using Ring = typename T::Ring;
+  const SmemPlan plan = plan_smem(sh, kTier);
+  Ctl* ctl = reinterpret_cast<Ctl*>(smem + plan.ctl_off);
+  Round<kTier> c;
   c.d = &d;
-  c.agents = d.agents;
-  c.vslot = d.vslot;
+  c.ctl = ctl;
+  c.aring = reinterpret_cast<Ring*>(smem + plan.aring_off);
+  c.vring = reinterpret_cast<Ring*>(smem + plan.vring_off);
+  c.amask = sh.ring_a - 1;
+  c.vmask = sh.ring_v - 1;
   c.pair = pair;
   c.rules = rules;
-  c.n_labels = n_labels;
-  c.lo_a = c.hi_a = c.lo_v = c.hi_v = 0;
+  c.n_labels = sh.n_labels;
+  void* q0;
+  uint32_t qstride;  // queue buffer stride in items
+  if constexpr (T::kAgentsSmem) {
+    c.agents = reinterpret_cast<uint4*>(smem + plan.agents_off);
+    c.cap_agents = sh.res_agents;
+  } else {
+    c.agents = d.agents;
+    c.cap_agents = d.cap_agents;
+  }
+  if constexpr (T::kSlotsSmem) {
+    c.vslot = smem + plan.slots_off;
+    c.cap_vars = sh.res_vars;
+    q0 = smem + plan.queue_off;
+    c.cap_queue = sh.res_queue;
+  } else {
+    c.vslot = d.vslot;
+    c.cap_vars = d.cap_vars;
+    q0 = d.queue;
+    c.cap_queue = d.cap_queue;
+  }
+  if constexpr (T::kPacked) c.cap_agents = min(c.cap_agents, 65535u);
+  qstride = c.cap_queue;
+  // ---- init: private copy of the input agents, empty slots, zero counters
+  const bool fits = d.n_in_agents <= c.cap_agents && d.n_in_vars <= c.cap_vars;
+  for (uint32_t i = threadIdx.x; i < c.cap_vars; i += blockDim.x) c.vslot[i] = kNone;
+  if (fits)
+    for (uint32_t i = threadIdx.x; i < d.n_in_agents; i += blockDim.x) c.agents[i] = d.in_agents[i];
+  {
+    uint32_t* w = reinterpret_cast<uint32_t*>(ctl);
+    for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += blockDim.x) w[i] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->agent_bump = d.n_in_agents;
+    ctl->var_bump = d.n_in_vars;
+    ctl->hdr.n = d.n_in_eqs;
+    ctl->t_prev = globaltimer();
+    ctl->rounds = 1;
+    if (!fits) {
+      ctl->err_code = INET_ERR_ARENA;
+      ctl->hdr.stop = 1;
+    } else if (d.n_in_eqs == 0) {  // one no-op loop (engine.py:222-223)
+      ctl->hdr.stop = 1;
+      if (d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
+    } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207)
+      ctl->err_code = INET_ERR_LOOP_CAP;
+      ctl->hdr.stop = 1;
+    }
+  }
+  __syncthreads();
   c.failed = false;
-  // thread-0 bookkeeping
-  unsigned long long t_prev = 0, tot_i = 0, tot_c = 0;
-  int32_t parked_total = 0;
-  uint32_t r = 1;
-  for (;; ++r) {
-    const RoundCtr* prev = &ctl->ctr[(r - 1) % 3];
-    const uint32_t n = vload(&prev->qcount);
-    const uint32_t p_atake = vload(&prev->atake), p_afree = vload(&prev->afree);
-    const uint32_t p_vtake = vload(&prev->vtake), p_vfree = vload(&prev->vfree);
-    c.lo_a += min(p_atake, c.hi_a - c.lo_a);
-    c.hi_a += p_afree;
-    c.lo_v += min(p_vtake, c.hi_v - c.lo_v);
-    c.hi_v += p_vfree;
-    // errors of round r-1 are read from its (now frozen) counters so that
-    // every thread takes the same exit at the same round
-    const uint32_t err = vload(&prev->err);
-    if (threadIdx.x == 0) {
-      const unsigned long long now = globaltimer();
-      if (r > 1) {
-        const uint32_t pi = vload(&prev->ints), pc = vload(&prev->comms);
-        parked_total += static_cast<int32_t>(vload(reinterpret_cast<const uint32_t*>(&prev->parked)));
-        tot_i += pi;
-        tot_c += pc;
-        if (d.stats && r - 2 < d.cap_rounds)
-          d.stats[r - 2] = make_uint4(pi, pc, n + static_cast<uint32_t>(parked_total),
-                                      static_cast<uint32_t>(now - t_prev));
-      }
-      t_prev = now;
-      RoundCtr* nxt = &ctl->ctr[(r + 1) % 3];
-      *nxt = RoundCtr{};
-    }
-    if (err) break;
-    if (r > max_rounds) {  // engine.py:205-207
-      if (threadIdx.x == 0) atomicCAS(&ctl->err, 0u, static_cast<uint32_t>(INET_ERR_LOOP_CAP));
-      break;
-    }
-    if (n == 0) {
-      // the trailing no-op loop the reference records (engine.py:222-223)
-      if (threadIdx.x == 0 && d.stats && r - 1 < d.cap_rounds)
-        d.stats[r - 1] = make_uint4(0, 0, static_cast<uint32_t>(parked_total), 0);
-      break;
-    }
-    c.cur = &ctl->ctr[r % 3];
-    const uint2* in = d.queue + ((r - 1) & 1u) * d.cap_queue;
-    c.out = d.queue + (r & 1u) * d.cap_queue;
+  c.cur = &ctl->ctr;
+  const uint32_t n_warps = (blockDim.x + 31u) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t r = 1;; ++r) {
+    const Header h = ctl->hdr;
+    if (h.stop) break;
+    const uint32_t n = h.n;
+    c.lo_a = h.lo_a;
+    c.hi_a = h.hi_a;
+    c.lo_v = h.lo_v;
+    c.hi_v = h.hi_v;
     c.ints = c.comms = 0;
     c.parked = 0;
-    for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
-      const uint2 eq = in[i];
-      if (((eq.x | eq.y) & kVar) == 0)
+    if (r == 1) {
+      // the input equations, in any class (communication_phase's first pass)
+      c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + qstride)
+                         : static_cast<void*>(static_cast<uint2*>(q0) + qstride);
+      for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
+        const uint2 eq = d.in_eqs[i];
+        if (((eq.x | eq.y) & kVar) == 0)
+          interact(c, eq.x, eq.y);
+        else
+          link(c, eq.x, eq.y);
+      }
+    } else if constexpr (T::kPacked) {
+      const uint32_t* in = static_cast<const uint32_t*>(q0) + ((r - 1) & 1u) * qstride;
+      c.out = static_cast<uint32_t*>(q0) + (r & 1u) * qstride;
+      for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
+        const uint32_t w = in[i];
+        interact(c, w >> 16, w & 0xFFFFu);
+      }
+    } else {
+      const uint2* in = static_cast<const uint2*>(q0) + ((r - 1) & 1u) * qstride;
+      c.out = static_cast<uint2*>(q0) + (r & 1u) * qstride;
+      for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
+        const uint2 eq = in[i];
         interact(c, eq.x, eq.y);
-      else
-        link(c, eq.x, eq.y);  // round 1 only: input equations that are not active
+      }
     }
     const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
     const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
     const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
-    if ((threadIdx.x & 31u) == 0) {
+    __syncwarp();
+    uint32_t last = 0;
+    if (lane == 0) {
       if (wi) atomicAdd(&c.cur->ints, wi);
       if (wc) atomicAdd(&c.cur->comms, wc);
       if (wp) atomicAdd(&c.cur->parked, wp);
+      __threadfence_block();
+      last = atomicAdd(&ctl->done_warps, 1u) == n_warps - 1;
+    }
+    if (last) {
+      // every other warp has finished round r: close it and open round r+1
+      __threadfence_block();
+      RoundCtr k;
+      {
+        const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(&ctl->ctr);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&k);
+#pragma unroll
+        for (int i = 0; i < static_cast<int>(sizeof(RoundCtr) / 4); ++i) dst[i] = src[i];
+      }
+      Header nh;
+      nh.pad[0] = nh.pad[1] = 0;
+      // frees of round r were kept while they fit the ring (against its old window)
+      const uint32_t wa = min(k.afree, sh.ring_a - (h.hi_a - h.lo_a));
+      const uint32_t wv = min(k.vfree, sh.ring_v - (h.hi_v - h.lo_v));
+      nh.lo_a = h.lo_a + min(k.atake, h.hi_a - h.lo_a);
+      nh.hi_a = h.hi_a + wa;
+      nh.lo_v = h.lo_v + min(k.vtake, h.hi_v - h.lo_v);
+      nh.hi_v = h.hi_v + wv;
+      nh.n = k.qcount;
+      nh.stop = 0;
+      const int32_t parked = ctl->parked_total + k.parked;
+      ctl->parked_total = parked;
+      ctl->tot_i += k.ints;
+      ctl->tot_c += k.comms;
+      const unsigned long long now = globaltimer();
+      if (d.stats && r - 1 < d.cap_rounds)
+        d.stats[r - 1] = make_uint4(k.ints, k.comms, k.qcount + static_cast<uint32_t>(parked),
+                                    static_cast<uint32_t>(now - ctl->t_prev));
+      ctl->t_prev = now;
+      ctl->rounds = r + 1;
+      if (k.err) {
+        nh.stop = 1;
+      } else if (k.qcount == 0) {
+        // the trailing no-op loop the reference records (engine.py:222-223)
+        nh.stop = 1;
+        if (d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked), 0);
+      } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
+        nh.stop = 1;
+        atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_LOOP_CAP));
+      }
+      ctl->ctr = RoundCtr{};
+      ctl->hdr = nh;
+      ctl->done_warps = 0;
     }
     __syncthreads();
   }
-  // residual parked equations, in variable-id order
   __syncthreads();
-  const uint32_t hw = min(vload(&ctl->var_bump), d.cap_vars);
+  // ---- results: residual parked equations in variable-id order, arena copy
+  const uint32_t hw = min(ctl->var_bump, c.cap_vars);
   uint32_t base = 0;
   for (uint32_t c0 = 0; c0 < hw; c0 += blockDim.x) {
     const uint32_t x = c0 + threadIdx.x;
-    const uint32_t v = x < hw ? d.vslot[x] : kNone;
+    const uint32_t v = x < hw ? c.vslot[x] : kNone;
     uint32_t off;
-    const uint32_t tot = block_scan_flag(v != kNone, scratch, &off);
-    if (v != kNone) d.residual[base + off] = make_uint2(kVar | x, v);
+    const uint32_t tot = block_scan_flag(v != kNone, ctl->scratch, &off);
+    if (v != kNone && base + off < d.cap_vars) d.residual[base + off] = make_uint2(kVar | x, v);
     base += tot;
   }
-  if (threadIdx.x == 0) {
-    ctl->rounds = r;
-    ctl->interactions = tot_i;
-    ctl->communications = tot_c;
-    ctl->n_residual = base;
-    ctl->parked_total = static_cast<uint32_t>(parked_total);
+  const uint32_t ahw = min(ctl->agent_bump, c.cap_agents);
+  if constexpr (T::kAgentsSmem) {
+    const uint32_t n_copy = min(ahw, d.cap_agents);
+    for (uint32_t i = threadIdx.x; i < n_copy; i += blockDim.x) d.agents[i] = c.agents[i];
   }
+  if (threadIdx.x == 0) {
+    NetCtl* g = d.ctl;
+    g->agent_bump = ahw;
+    g->var_bump = hw;
+    g->err = ctl->err_code;
+    g->err_a = ctl->err_a;
+    g->err_b = ctl->err_b;
+    g->rounds = ctl->rounds;
+    g->interactions = ctl->tot_i;
+    g->communications = ctl->tot_c;
+    g->n_residual = base;
+    g->parked_total = static_cast<uint32_t>(ctl->parked_total);
+    if ((ahw > d.cap_agents || hw > d.cap_vars) && g->err == 0) g->err = INET_ERR_ARENA;
+  }
+  __syncthreads();
 }
 
 }  // namespace inetdev

@@ -22,49 +22,52 @@ using inetdev::NetDesc;
 
 namespace {
 
-constexpr uint32_t kScratchWords = 33;
+using inetdev::Shape;
 
-template <int kBlock>
+using inetdev::kTierG;
+using inetdev::kTierM;
+using inetdev::kTierS;
+using inetdev::plan_smem;
+
+template <int kBlock, int kTier>
 __global__ void __launch_bounds__(kBlock) reduce_kernel(const NetDesc* __restrict__ nets, uint32_t n_nets,
-                                                        const uint32_t* __restrict__ blob, uint32_t max_rounds) {
-  extern __shared__ uint32_t smem[];
+                                                        const uint32_t* __restrict__ blob, Shape sh) {
+  extern __shared__ __align__(16) uint32_t smem[];
   __shared__ NetDesc sd;
-  __shared__ uint32_t scratch[kScratchWords];
-  const uint32_t n_labels = blob[1], n_rules = blob[2];
-  const uint32_t pair_words = (n_labels * n_labels + 1) / 2;
-  const uint32_t words = pair_words + n_rules * inetdev::kRuleWords;
-  for (uint32_t i = threadIdx.x; i < words; i += kBlock) smem[i] = blob[4 + i];
+  for (uint32_t i = threadIdx.x; i < sh.rule_words; i += kBlock) smem[i] = blob[4 + i];
+  const uint32_t pair_words = (sh.n_labels * sh.n_labels + 1) / 2;
   const uint16_t* pair = reinterpret_cast<const uint16_t*>(smem);
   const uint32_t* rules = smem + pair_words;
   for (uint32_t net = blockIdx.x; net < n_nets; net += gridDim.x) {
     __syncthreads();
     if (threadIdx.x == 0) sd = nets[net];
     __syncthreads();
-    inetdev::run_net(sd, pair, rules, n_labels, max_rounds, scratch);
+    inetdev::run_net<kTier>(sd, sh, pair, rules, smem);
   }
 }
 
-using KernelFn = void (*)(const NetDesc*, uint32_t, const uint32_t*, uint32_t);
+using KernelFn = void (*)(const NetDesc*, uint32_t, const uint32_t*, Shape);
 
-KernelFn pick_kernel(uint32_t threads) {
+template <int kTier>
+KernelFn pick_kernel_t(uint32_t threads) {
   switch (threads) {
     case 64:
-      return reduce_kernel<64>;
+      return reduce_kernel<64, kTier>;
     case 128:
-      return reduce_kernel<128>;
+      return reduce_kernel<128, kTier>;
     case 256:
-      return reduce_kernel<256>;
+      return reduce_kernel<256, kTier>;
     case 512:
-      return reduce_kernel<512>;
+      return reduce_kernel<512, kTier>;
     default:
-      return reduce_kernel<1024>;
+      return reduce_kernel<1024, kTier>;
   }
 }
 
-uint32_t pow2_at_least(uint32_t v) {
-  uint32_t p = 1;
-  while (p < v) p <<= 1;
-  return p;
+KernelFn pick_kernel(uint32_t threads, int tier) {
+  if (tier == kTierS) return pick_kernel_t<kTierS>(threads);
+  if (tier == kTierM) return pick_kernel_t<kTierM>(threads);
+  return pick_kernel_t<kTierG>(threads);
 }
 
 }  // namespace
@@ -107,7 +110,9 @@ struct inet_ctx {
   bool count_rules = false;
   std::vector<uint32_t> h_hist;
   uint64_t io_h2d = 0, io_d2h = 0;
-  uint32_t cap_agents = 0, cap_vars = 0, cap_queue = 0, cap_rounds = 0, ring_a = 0, ring_v = 0;
+  uint32_t cap_agents = 0, cap_vars = 0, cap_queue = 0, cap_rounds = 0;
+  int tier = kTierG;  // tier of the last successful run
+  Shape shape{};
   bool collect_stats = false;
   bool reduced = false;
   // results (host)
@@ -260,19 +265,16 @@ int upload_input(inet_ctx* c) {
   return INET_OK;
 }
 
-// Size the per-net slabs and write the descriptor table.
-int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_rounds) {
+// Size the per-net global slabs and write the descriptor table.
+int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_queue, uint32_t cap_rounds) {
   const uint32_t n = c->n_nets;
   c->cap_agents = cap_agents;
   c->cap_vars = cap_vars;
-  c->cap_queue = cap_agents / 2 + c->max_in_eqs + 1;
+  c->cap_queue = cap_queue;
   c->cap_rounds = cap_rounds;
-  c->ring_a = pow2_at_least(cap_agents);
-  c->ring_v = pow2_at_least(cap_vars);
   const size_t N = n;
   if (c->d_agents.ensure(N * cap_agents * 16) || c->d_vslot.ensure(N * cap_vars * 4) ||
-      c->d_aring.ensure(N * c->ring_a * 4) || c->d_vring.ensure(N * c->ring_v * 4) ||
-      c->d_queue.ensure(N * 2 * c->cap_queue * 8) || c->d_resid.ensure(N * cap_vars * 8) ||
+      c->d_queue.ensure(N * 2 * cap_queue * 8) || c->d_resid.ensure(N * cap_vars * 8) ||
       c->d_ctl.ensure(N * sizeof(NetCtl)) || c->d_desc.ensure(N * sizeof(NetDesc)) ||
       (cap_rounds && c->d_stats.ensure(N * cap_rounds * 16)) ||
       (c->count_rules && c->d_hist.ensure(N * std::max(c->n_rules, 1u) * 4)))
@@ -284,19 +286,15 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_rou
     std::memset(&d, 0, sizeof(d));
     d.agents = static_cast<uint4*>(c->d_agents.p) + size_t(i) * cap_agents;
     d.vslot = static_cast<uint32_t*>(c->d_vslot.p) + size_t(i) * cap_vars;
-    d.aring = static_cast<uint32_t*>(c->d_aring.p) + size_t(i) * c->ring_a;
-    d.vring = static_cast<uint32_t*>(c->d_vring.p) + size_t(i) * c->ring_v;
-    d.queue = static_cast<uint2*>(c->d_queue.p) + size_t(i) * 2 * c->cap_queue;
+    d.queue = static_cast<uint2*>(c->d_queue.p) + size_t(i) * 2 * cap_queue;
     d.stats = cap_rounds ? static_cast<uint4*>(c->d_stats.p) + size_t(i) * cap_rounds : nullptr;
     d.residual = static_cast<uint2*>(c->d_resid.p) + size_t(i) * cap_vars;
     d.ctl = static_cast<NetCtl*>(c->d_ctl.p) + i;
     d.rule_hist = c->count_rules ? static_cast<uint32_t*>(c->d_hist.p) + size_t(i) * std::max(c->n_rules, 1u) : nullptr;
     d.cap_agents = cap_agents;
     d.cap_vars = cap_vars;
-    d.cap_queue = c->cap_queue;
+    d.cap_queue = cap_queue;
     d.cap_rounds = cap_rounds;
-    d.amask = c->ring_a - 1;
-    d.vmask = c->ring_v - 1;
     d.in_agents = static_cast<const uint4*>(c->d_in_agents.p) + c->agent_off[i];
     d.in_eqs = static_cast<const uint2*>(c->d_in_eqs.p) + c->eq_off[i];
     d.n_in_agents = static_cast<uint32_t>(c->agent_off[i + 1] - c->agent_off[i]);
@@ -321,29 +319,37 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
   return c->n_nets >= 16 ? 512 : 1024;
 }
 
-// One attempt at the current capacities: init + reduce kernel, timed.
-int launch(inet_ctx* c, const inet_cfg* cfg, float* ms) {
+// One attempt at the current capacities and tier: one kernel launch, timed.
+int launch(inet_ctx* c, const inet_cfg* cfg, const Shape& sh, int tier, float* ms) {
   const uint32_t threads = auto_threads(c, cfg);
-  KernelFn fn = pick_kernel(threads);
-  if (c->smem_bytes > 48 * 1024) {
-    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(c->smem_bytes)));
-  }
-  const uint32_t max_rounds = cfg ? cfg->max_loops : 1000000u;
-  int dev_sms = 0;
+  KernelFn fn = pick_kernel(threads, tier);
+  const size_t smem = size_t(plan_smem(sh, tier).words) * 4;
+  int dev_sms = 0, max_optin = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  if (smem + sizeof(NetDesc) > size_t(max_optin)) return INET_ERR_UNSUPPORTED;
+  CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), c->smem_bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), smem);
   uint32_t grid = std::max(1, dev_sms * std::max(per_sm, 1));
   grid = std::min(grid, c->n_nets);
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-  fn<<<grid, threads, c->smem_bytes, c->stream>>>(static_cast<const NetDesc*>(c->d_desc.p), c->n_nets,
-                                                  static_cast<const uint32_t*>(c->d_blob.p), max_rounds);
+  fn<<<grid, threads, smem, c->stream>>>(static_cast<const NetDesc*>(c->d_desc.p), c->n_nets,
+                                         static_cast<const uint32_t*>(c->d_blob.p), sh);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
   CUDA_TRY(cudaEventSynchronize(c->ev1));
   CUDA_TRY(cudaEventElapsedTime(ms, c->ev0, c->ev1));
   return INET_OK;
+}
+
+Shape base_shape(const inet_ctx* c, uint32_t max_loops) {
+  Shape sh{};
+  sh.max_rounds = max_loops;
+  sh.rule_words = static_cast<uint32_t>(c->blob.size() - 4);
+  sh.n_labels = c->n_labels;
+  return sh;
 }
 
 int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
@@ -358,28 +364,73 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   c->count_rules = cfg && cfg->count_rules;
   uint32_t cap_rounds = 0;
   if (c->collect_stats) cap_rounds = std::min<uint32_t>(max_loops + 1u, 1u << 22);
-  // initial capacities: enough for the inputs plus headroom
+  const uint32_t retries = cfg && cfg->max_retries ? cfg->max_retries : 8;
+  float ms = 0;
+  c->ctl.assign(c->n_nets, NetCtl{});
+  auto any_oom = [&]() {
+    for (uint32_t i = 0; i < c->n_nets; ++i)
+      if (c->ctl[i].err == INET_ERR_ARENA) return true;
+    return false;
+  };
+  auto fetch_ctl = [&]() -> int {
+    CUDA_TRY(cudaMemcpy(c->ctl.data(), c->d_ctl.p, c->n_nets * sizeof(NetCtl), cudaMemcpyDeviceToHost));
+    c->io_d2h += c->n_nets * sizeof(NetCtl);
+    c->io_h2d += c->n_nets * sizeof(NetDesc);
+    return INET_OK;
+  };
+  const bool user_caps = cfg && (cfg->cap_agents || cfg->cap_vars);
+  bool done = false;
+  // Try the shared-memory tiers first; a net that overflows sends the whole
+  // launch to the next tier (S or M, then G with doubling capacities).
+  auto attempt_tier = [&](int tier, const Shape& sh, uint32_t ca, uint32_t cv, uint32_t cq) -> int {
+    int st = layout(c, ca, cv, cq, cap_rounds);
+    if (st) return st;
+    st = launch(c, cfg, sh, tier, &ms);
+    if (st) return st;
+    fetch_ctl();
+    c->tier = tier;
+    c->shape = sh;
+    return INET_OK;
+  };
+  if (!user_caps && c->n_nets > 1 && c->max_in_agents <= 512 && c->max_in_vars <= 512) {
+    for (uint32_t cap : {1024u, 2048u}) {
+      Shape sh = base_shape(c, max_loops);
+      sh.res_agents = cap;
+      sh.res_vars = cap;
+      sh.res_queue = cap / 2;
+      sh.ring_a = cap;
+      sh.ring_v = cap;
+      int st = attempt_tier(kTierS, sh, sh.res_agents, sh.res_vars, 1);
+      if (st == INET_OK && !any_oom()) {
+        done = true;
+        break;
+      }
+      if (st != INET_OK && st != INET_ERR_UNSUPPORTED) return st;
+    }
+  }
+  if (!done && !user_caps && c->n_nets <= 148 && c->max_in_agents < 32768 && c->max_in_vars < 16384) {
+    Shape sh = base_shape(c, max_loops);
+    sh.res_vars = 16384;
+    sh.res_queue = 8192;
+    sh.ring_a = 16384;
+    sh.ring_v = 16384;
+    int st = attempt_tier(kTierM, sh, 65535, sh.res_vars, 1);
+    if (st == INET_OK && !any_oom()) done = true;
+    else if (st != INET_OK && st != INET_ERR_UNSUPPORTED) return st;
+  }
   uint32_t ca = cfg && cfg->cap_agents ? cfg->cap_agents : 0;
   uint32_t cv = cfg && cfg->cap_vars ? cfg->cap_vars : 0;
   if (!ca) ca = c->n_nets == 1 ? (1u << 20) : 4096u;
   if (!cv) cv = c->n_nets == 1 ? (1u << 20) : 8192u;
   ca = std::max(ca, c->max_in_agents + 64);
   cv = std::max(cv, c->max_in_vars + 64);
-  const uint32_t retries = cfg && cfg->max_retries ? cfg->max_retries : 8;
-  float ms = 0;
-  c->ctl.assign(c->n_nets, NetCtl{});
-  for (uint32_t attempt = 0;; ++attempt) {
-    int st = layout(c, ca, cv, cap_rounds);
+  for (uint32_t attempt = 0; !done; ++attempt) {
+    Shape sh = base_shape(c, max_loops);
+    sh.ring_a = c->n_nets == 1 ? 8192 : 1024;
+    sh.ring_v = c->n_nets == 1 ? 8192 : 1024;
+    int st = attempt_tier(kTierG, sh, ca, cv, ca / 2 + 1);
     if (st) return st;
-    st = launch(c, cfg, &ms);
-    if (st) return st;
-    CUDA_TRY(cudaMemcpy(c->ctl.data(), c->d_ctl.p, c->n_nets * sizeof(NetCtl), cudaMemcpyDeviceToHost));
-    c->io_d2h += c->n_nets * sizeof(NetCtl);
-    c->io_h2d += c->n_nets * sizeof(NetDesc);
-    bool oom = false;
-    for (uint32_t i = 0; i < c->n_nets; ++i) oom |= c->ctl[i].err == INET_ERR_ARENA;
-    if (!oom || attempt + 1 >= retries) break;
-    // grow: agents and variables double (queue follows agents)
+    if (!any_oom() || attempt + 1 >= retries) break;
     if (uint64_t(ca) * 2 >= INET_VAR_BIT || uint64_t(cv) * 2 >= INET_VAR_BIT) break;
     ca *= 2;
     cv *= 2;
@@ -401,6 +452,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     s.n_residual = k.n_residual;
     s.cap_agents = c->cap_agents;
     s.cap_vars = c->cap_vars;
+    s.tier = static_cast<uint32_t>(c->tier);
     if (first == INET_OK && k.err) first = static_cast<int>(k.err);
   }
   c->reduced = true;
@@ -462,17 +514,17 @@ int inet_batch_reduce(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
 
 int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
   if (!c || !c->reduced) return INET_ERR_STATE;
-  // capacities of the successful run are reused: no retry growth expected
+  // same tier, shape and capacities as the successful run: no growth expected
   inet_cfg k = cfg ? *cfg : inet_cfg{1000000u, 0, 0, 0, 0, 0, 0, 0};
   c->count_rules = k.count_rules != 0;
-  k.cap_agents = c->cap_agents;
-  k.cap_vars = c->cap_vars;
   CUDA_TRY(cudaSetDevice(c->device));
   const uint32_t cap_rounds = (k.collect_stats) ? std::min<uint32_t>(k.max_loops + 1u, 1u << 22) : 0;
-  int st = layout(c, c->cap_agents, c->cap_vars, cap_rounds);
+  int st = layout(c, c->cap_agents, c->cap_vars, c->cap_queue, cap_rounds);
   if (st) return st;
+  Shape sh = c->shape;
+  sh.max_rounds = k.max_loops;
   float ms = 0;
-  st = launch(c, &k, &ms);
+  st = launch(c, &k, sh, c->tier, &ms);
   if (st) return st;
   if (device_ms) *device_ms = ms;
   return INET_OK;

@@ -1,0 +1,27 @@
+"""One reduction of a named workload (for ncu captures; prints nothing timed)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1404_0076_b200 import EngineConfig, _native, engine  # noqa: E402
+from paper_1404_0076_b200.programs import program  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="a38")
+ap.add_argument("--nets", type=int, default=4096)
+ap.add_argument("--threads", type=int, default=0)
+ap.add_argument("--repeat", type=int, default=1)
+a = ap.parse_args()
+spec = {"a38": ("ackermann", (3, 8), 1), "a310": ("ackermann", (3, 10), 1), "fib18": ("fibonacci", (18,), 1),
+        "batch": ("ackermann", (3, 6), a.nets)}[a.workload]
+p = program(spec[0])
+prep = engine.prepare([p.build_input(*spec[1]) for _ in range(spec[2])], p.rules)
+ctx = _native.Context(0)
+ctx.load_rules(prep.blob)
+ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
+k = engine.native_cfg(EngineConfig(collect_stats=False, threads=a.threads))
+for _ in range(a.repeat):
+    code, ms = ctx.reduce(k)
+    st = ctx.stats(0)
+    print(a.workload, "code", code, "ms", ms, ctx.totals(), "tier", st.tier, "hw", st.agent_hw, st.var_hw)
