@@ -15,7 +15,8 @@ import numpy as np
 
 from .errors import DeviceError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libinetb200.so")
+LIB_PATH = os.environ.get("INET_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                             "libinetb200.so")
 
 OK, NO_RULE, LOOP_CAP, ARENA, CUDA, ARG, UNSUPPORTED, NO_DEVICE, STATE = range(9)
 

@@ -52,7 +52,7 @@ constexpr uint32_t kNone = INET_NONE;
 constexpr int kEnvFresh = 6;
 constexpr int kEnvNew = 14;
 constexpr int kEnvNone = 22;
-constexpr int kEnvSize = 24;
+constexpr int kEnvSize = 23;  // sources 0..22 (22 = none)
 constexpr int kRuleWords = 16;
 constexpr int kFastEq = 4;  // rhs equations linked with overlapped exchanges
 
@@ -61,6 +61,8 @@ enum : int { kTierS = 0, kTierM = 1, kTierG = 2 };
 template <int kTier>
 struct Traits {
   using Ring = uint16_t;
+  static constexpr bool kEnvSmem = false;           // per-thread source table in shared memory
+  static constexpr bool kEnvLocal = kTier == kTierS;  // per-thread source table in local memory (L1)
   static constexpr bool kAgentsSmem = kTier == kTierS;
   static constexpr bool kSlotsSmem = true;
   static constexpr bool kPacked = true;
@@ -68,6 +70,8 @@ struct Traits {
 template <>
 struct Traits<kTierG> {
   using Ring = uint32_t;
+  static constexpr bool kEnvSmem = false;
+  static constexpr bool kEnvLocal = false;
   static constexpr bool kAgentsSmem = false;
   static constexpr bool kSlotsSmem = false;
   static constexpr bool kPacked = false;
@@ -154,6 +158,8 @@ struct Shape {
   uint32_t max_rounds;
   uint32_t rule_words;            // pair table + rule records (words)
   uint32_t n_labels;
+  uint32_t threads;               // CTA size
+  uint32_t pad;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -161,6 +167,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+
+#ifdef INET_TIMING
+// Development build only: per-phase clock64 totals (tools/phase_timing.py).
+#define INET_TMARK(c, k)                  \
+  do {                                    \
+    const long long _t = clock64();       \
+    (c).tm[k] += _t - (c).tlast;          \
+    (c).tlast = _t;                       \
+  } while (0)
+#else
+#define INET_TMARK(c, k) \
+  do {                   \
+  } while (0)
+#endif
 
 template <class T>
 __device__ __forceinline__ T vload(const T* p) {
@@ -177,6 +197,7 @@ struct Round {
   uint32_t* vslot;
   Ring* aring;
   Ring* vring;
+  uint32_t* env;  // this thread's column of the shared source table (stride blockDim)
   void* out;
   RoundCtr* cur;
   const uint16_t* pair;
@@ -188,6 +209,10 @@ struct Round {
   uint32_t ints, comms;
   int32_t parked;
   bool failed;
+#ifdef INET_TIMING
+  long long tm[8];
+  long long tlast;
+#endif
 };
 
 template <int kTier>
@@ -200,41 +225,46 @@ __device__ __forceinline__ void fail(Round<kTier>& c, uint32_t code, uint32_t a 
   }
 }
 
+// A contiguous claim on a free ring: ids j < got are ring[(pos + j) & mask],
+// the rest come from the bump pointer (bump + j - got).
+struct Claim {
+  uint32_t pos, got, bump;
+};
+
 template <int kTier>
-__device__ __forceinline__ bool alloc_vars(Round<kTier>& c, uint32_t nf, uint32_t* out) {
+__device__ __forceinline__ bool alloc_vars(Round<kTier>& c, uint32_t nf, Claim& k) {
+  k.pos = k.got = k.bump = 0;
   if (nf == 0) return true;
   const uint32_t t = atomicAdd(&c.cur->vtake, nf);
   const uint32_t avail = c.hi_v - c.lo_v;
-  uint32_t got = 0;
-  if (t < avail) got = min(avail - t, nf);
-  for (uint32_t j = 0; j < got; ++j) out[j] = kVar | c.vring[(c.lo_v + t + j) & c.vmask];
-  if (got < nf) {
-    const uint32_t need = nf - got;
-    const uint32_t b = atomicAdd(&c.ctl->var_bump, need);
-    if (b + need > c.cap_vars) {
+  k.pos = c.lo_v + t;
+  if (t < avail) k.got = min(avail - t, nf);
+  if (k.got < nf) {
+    const uint32_t need = nf - k.got;
+    k.bump = atomicAdd(&c.ctl->var_bump, need);
+    if (k.bump + need > c.cap_vars) {
       fail(c, INET_ERR_ARENA, 1);
       return false;
     }
-    for (uint32_t j = 0; j < need; ++j) out[got + j] = kVar | (b + j);
   }
   return true;
 }
 
 template <int kTier>
-__device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, uint32_t* out) {
+__device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, Claim& k) {
+  k.pos = k.got = k.bump = 0;
+  if (n == 0) return true;
   const uint32_t t = atomicAdd(&c.cur->atake, n);
   const uint32_t avail = c.hi_a - c.lo_a;
-  uint32_t got = 0;
-  if (t < avail) got = min(avail - t, n);
-  for (uint32_t j = 0; j < got; ++j) out[j] = c.aring[(c.lo_a + t + j) & c.amask];
-  if (got < n) {
-    const uint32_t need = n - got;
-    const uint32_t b = atomicAdd(&c.ctl->agent_bump, need);
-    if (b + need > c.cap_agents) {
+  k.pos = c.lo_a + t;
+  if (t < avail) k.got = min(avail - t, n);
+  if (k.got < n) {
+    const uint32_t need = n - k.got;
+    k.bump = atomicAdd(&c.ctl->agent_bump, need);
+    if (k.bump + need > c.cap_agents) {
       fail(c, INET_ERR_ARENA, 0);
       return false;
     }
-    for (uint32_t j = 0; j < need; ++j) out[got + j] = b + j;
   }
   return true;
 }
@@ -321,9 +351,11 @@ __device__ __forceinline__ void link(Round<kTier>& c, uint32_t l, uint32_t r) {
 // Rewrite one active pair (find_rule + instantiate, core.py:281-312).
 template <int kTier>
 __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r) {
+  INET_TMARK(c, 0);
   uint4 A = c.agents[l];
   uint4 B = c.agents[r];
   const uint32_t t = c.pair[A.x * c.n_labels + B.x];
+  INET_TMARK(c, 1);
   if (t == 0xFFFFu) {
     fail(c, INET_ERR_NO_RULE, A.x, B.x);
     return;
@@ -340,25 +372,73 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
   const uint32_t* R = c.rules + (t >> 1) * kRuleWords;
   const uint32_t hdr = R[0];
   const uint32_t nn = hdr & 0xFFu, ne = (hdr >> 8) & 0xFFu, nf = (hdr >> 16) & 0xFFu;
-  uint32_t env[kEnvSize];
-  env[0] = A.y;
-  env[1] = A.z;
-  env[2] = A.w;
-  env[3] = B.y;
-  env[4] = B.z;
-  env[5] = B.w;
-  env[kEnvNone] = kNone;
-  if (!alloc_vars(c, nf, env + kEnvFresh)) return;
-  env[kEnvNew] = l;
-  env[kEnvNew + 1] = r;
-  if (nn > 2 && !alloc_agents(c, nn - 2, env + kEnvNew + 2)) return;
+  Claim fv, na;
+  if (!alloc_vars(c, nf, fv)) return;
+  if (!alloc_agents(c, nn > 2 ? nn - 2 : 0, na)) return;
+  INET_TMARK(c, 2);
+  auto fresh = [&](uint32_t j) -> uint32_t {
+    return kVar | (j < fv.got ? static_cast<uint32_t>(c.vring[(fv.pos + j) & c.vmask]) : fv.bump + (j - fv.got));
+  };
+  auto extra = [&](uint32_t q) -> uint32_t {
+    return q < na.got ? static_cast<uint32_t>(c.aring[(na.pos + q) & c.amask]) : na.bump + (q - na.got);
+  };
+  uint32_t env_l[Traits<kTier>::kEnvLocal ? kEnvSize : 1];
+  if constexpr (Traits<kTier>::kEnvLocal) {
+    // Small nets (tier S): a per-thread table in local memory; with several
+    // CTAs per SM this measured faster than resolving sources by branches.
+    env_l[0] = A.y;
+    env_l[1] = A.z;
+    env_l[2] = A.w;
+    env_l[3] = B.y;
+    env_l[4] = B.z;
+    env_l[5] = B.w;
+    for (uint32_t j = 0; j < nf; ++j) env_l[kEnvFresh + j] = fresh(j);
+    env_l[kEnvNew] = l;
+    env_l[kEnvNew + 1] = r;
+    for (uint32_t q = 0; q + 2 < nn; ++q) env_l[kEnvNew + 2 + q] = extra(q);
+    env_l[kEnvNone] = kNone;
+  }
+  if constexpr (Traits<kTier>::kEnvSmem) {
+    // Source table in shared memory, one column per thread: every rule source
+    // then resolves with a single LDS.
+    uint32_t* E = c.env;
+    const uint32_t bd = blockDim.x;
+    E[0] = A.y;
+    E[bd] = A.z;
+    E[2 * bd] = A.w;
+    E[3 * bd] = B.y;
+    E[4 * bd] = B.z;
+    E[5 * bd] = B.w;
+    for (uint32_t j = 0; j < nf; ++j) E[(kEnvFresh + j) * bd] = fresh(j);
+    E[kEnvNew * bd] = l;
+    E[(kEnvNew + 1) * bd] = r;
+    for (uint32_t q = 0; q + 2 < nn; ++q) E[(kEnvNew + 2 + q) * bd] = extra(q);
+  }
+  // Resolve a rule source (include/inet_b200.h) to a term ref.
+  auto src = [&](uint32_t s) -> uint32_t {
+    if constexpr (Traits<kTier>::kEnvSmem) {
+      return c.env[s * blockDim.x];
+    } else if constexpr (Traits<kTier>::kEnvLocal) {
+      return env_l[s];
+    } else {
+      if (s < 3) return s == 0 ? A.y : (s == 1 ? A.z : A.w);
+      if (s < 6) return s == 3 ? B.y : (s == 4 ? B.z : B.w);
+      if (s < 14) return fresh(s - kEnvFresh);
+      if (s < 22) {
+        const uint32_t m = s - kEnvNew;
+        if (m < 2) return m == 0 ? l : r;
+        return extra(m - 2);
+      }
+      return kNone;
+    }
+  };
   for (uint32_t m = 0; m < nn; ++m) {
     const uint32_t w = R[1 + m];
-    c.agents[env[kEnvNew + m]] =
-        make_uint4(w & 0xFFu, env[(w >> 8) & 0xFFu], env[(w >> 16) & 0xFFu], env[w >> 24]);
+    c.agents[src(kEnvNew + m)] = make_uint4(w & 0xFFu, src((w >> 8) & 0xFFu), src((w >> 16) & 0xFFu), src(w >> 24));
   }
   if (nn < 2) free_agent(c, r);
   if (nn < 1) free_agent(c, l);
+  INET_TMARK(c, 3);
   // Link the rhs: issue the first exchange of every equation back to back so
   // their latencies overlap, then settle each.
   uint32_t xs[kFastEq], olds[kFastEq], vals[kFastEq];
@@ -367,7 +447,7 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
     xs[e] = kNone;
     if (e < static_cast<int>(ne)) {
       const uint32_t h = (R[9 + (e >> 1)] >> ((e & 1) * 16)) & 0xFFFFu;
-      const uint32_t el = env[h & 0xFFu], er = env[h >> 8];
+      const uint32_t el = src(h & 0xFFu), er = src(h >> 8);
       if (((el | er) & kVar) == 0) {
         push_active(c, el, er);
       } else {
@@ -383,9 +463,10 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
     if (xs[e] != kNone) settle(c, xs[e], olds[e], vals[e]);
   for (uint32_t e = kFastEq; e < ne; ++e) {
     const uint32_t h = (R[9 + (e >> 1)] >> ((e & 1) * 16)) & 0xFFFFu;
-    link(c, env[h & 0xFFu], env[h >> 8]);
+    link(c, src(h & 0xFFu), src(h >> 8));
   }
   c.ints += 1;
+  INET_TMARK(c, 4);
 }
 
 // Block-wide exclusive prefix of a 0/1 flag; returns the total.
@@ -415,7 +496,7 @@ __device__ __forceinline__ uint32_t block_scan_flag(bool flag, uint32_t* warp_to
 // Shared-memory plan (32-bit words):
 //   rule table | Ctl | agent ring | var ring | [S: agents] | [S,M: slots] | [S,M: 2 queues]
 struct SmemPlan {
-  uint32_t ctl_off, aring_off, vring_off, agents_off, slots_off, queue_off, words;
+  uint32_t ctl_off, aring_off, vring_off, agents_off, slots_off, queue_off, env_off, words;
 };
 
 __host__ __device__ inline uint32_t align4(uint32_t w) { return (w + 3u) & ~3u; }
@@ -429,7 +510,8 @@ __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
   p.agents_off = p.vring_off + align4((sh.ring_v * ring_bytes + 3) / 4);
   p.slots_off = p.agents_off + (tier == kTierS ? 4 * sh.res_agents : 0);
   p.queue_off = p.slots_off + (tier != kTierG ? align4(sh.res_vars) : 0);
-  p.words = p.queue_off + (tier != kTierG ? align4(2 * sh.res_queue) : 0);
+  p.env_off = p.queue_off + (tier != kTierG ? align4(2 * sh.res_queue) : 0);
+  p.words = p.env_off;  // (shared source table disabled: measured slower than registers)
   return p;
 }
 
@@ -503,6 +585,12 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   __syncthreads();
   c.failed = false;
   c.cur = &ctl->ctr;
+  c.env = smem + plan.env_off + threadIdx.x;
+  if constexpr (T::kEnvSmem) c.env[(kEnvSize - 1) * blockDim.x] = kNone;  // (disabled tier option)
+#ifdef INET_TIMING
+  for (int i = 0; i < 8; ++i) c.tm[i] = 0;
+  c.tlast = clock64();
+#endif
   const uint32_t n_warps = (blockDim.x + 31u) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
   for (uint32_t r = 1;; ++r) {
@@ -541,6 +629,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
         interact(c, eq.x, eq.y);
       }
     }
+    INET_TMARK(c, 5);
     const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
     const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
     const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
@@ -550,12 +639,16 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       if (wi) atomicAdd(&c.cur->ints, wi);
       if (wc) atomicAdd(&c.cur->comms, wc);
       if (wp) atomicAdd(&c.cur->parked, wp);
+#ifndef INET_NO_FENCE
       __threadfence_block();
+#endif
       last = atomicAdd(&ctl->done_warps, 1u) == n_warps - 1;
     }
     if (last) {
       // every other warp has finished round r: close it and open round r+1
+#ifndef INET_NO_FENCE
       __threadfence_block();
+#endif
       RoundCtr k;
       {
         const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(&ctl->ctr);
@@ -578,7 +671,11 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       ctl->parked_total = parked;
       ctl->tot_i += k.ints;
       ctl->tot_c += k.comms;
+#ifdef INET_NO_TIMER
+      const unsigned long long now = 0;
+#else
       const unsigned long long now = globaltimer();
+#endif
       if (d.stats && r - 1 < d.cap_rounds)
         d.stats[r - 1] = make_uint4(k.ints, k.comms, k.qcount + static_cast<uint32_t>(parked),
                                     static_cast<uint32_t>(now - ctl->t_prev));
@@ -598,8 +695,15 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       ctl->hdr = nh;
       ctl->done_warps = 0;
     }
+    INET_TMARK(c, 6);
     __syncthreads();
+    INET_TMARK(c, 7);
   }
+#ifdef INET_TIMING
+  if (d.rule_hist)
+    for (int i = 0; i < 8; ++i)
+      atomicAdd(reinterpret_cast<unsigned long long*>(d.rule_hist) + 32 + i, static_cast<unsigned long long>(c.tm[i]));
+#endif
   __syncthreads();
   // ---- results: residual parked equations in variable-id order, arena copy
   const uint32_t hw = min(ctl->var_bump, c.cap_vars);

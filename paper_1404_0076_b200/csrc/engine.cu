@@ -72,6 +72,10 @@ KernelFn pick_kernel(uint32_t threads, int tier) {
 
 }  // namespace
 
+// Words per net of the rule histogram (>= 128 so development builds can append
+// their phase timers after the counts).
+inline uint32_t hist_stride(const struct inet_ctx* c);
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -125,6 +129,8 @@ struct inet_ctx {
   std::vector<inethost::NormalForm> results;
   std::vector<uint8_t> finalized;
 };
+
+inline uint32_t hist_stride(const inet_ctx* c) { return std::max(c->n_rules, 128u); }
 
 #define CUDA_TRY(expr)                                                                         \
   do {                                                                                         \
@@ -277,9 +283,9 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
       c->d_queue.ensure(N * 2 * cap_queue * 8) || c->d_resid.ensure(N * cap_vars * 8) ||
       c->d_ctl.ensure(N * sizeof(NetCtl)) || c->d_desc.ensure(N * sizeof(NetDesc)) ||
       (cap_rounds && c->d_stats.ensure(N * cap_rounds * 16)) ||
-      (c->count_rules && c->d_hist.ensure(N * std::max(c->n_rules, 1u) * 4)))
+      (c->count_rules && c->d_hist.ensure(N * hist_stride(c) * 4)))
     return INET_ERR_CUDA;
-  if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * std::max(c->n_rules, 1u) * 4, c->stream));
+  if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * hist_stride(c) * 4, c->stream));
   std::vector<NetDesc> desc(n);
   for (uint32_t i = 0; i < n; ++i) {
     NetDesc& d = desc[i];
@@ -290,7 +296,7 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.stats = cap_rounds ? static_cast<uint4*>(c->d_stats.p) + size_t(i) * cap_rounds : nullptr;
     d.residual = static_cast<uint2*>(c->d_resid.p) + size_t(i) * cap_vars;
     d.ctl = static_cast<NetCtl*>(c->d_ctl.p) + i;
-    d.rule_hist = c->count_rules ? static_cast<uint32_t*>(c->d_hist.p) + size_t(i) * std::max(c->n_rules, 1u) : nullptr;
+    d.rule_hist = c->count_rules ? static_cast<uint32_t*>(c->d_hist.p) + size_t(i) * hist_stride(c) : nullptr;
     d.cap_agents = cap_agents;
     d.cap_vars = cap_vars;
     d.cap_queue = cap_queue;
@@ -320,8 +326,9 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
 }
 
 // One attempt at the current capacities and tier: one kernel launch, timed.
-int launch(inet_ctx* c, const inet_cfg* cfg, const Shape& sh, int tier, float* ms) {
+int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
   const uint32_t threads = auto_threads(c, cfg);
+  sh.threads = threads;
   KernelFn fn = pick_kernel(threads, tier);
   const size_t smem = size_t(plan_smem(sh, tier).words) * 4;
   int dev_sms = 0, max_optin = 0;
@@ -410,10 +417,10 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   }
   if (!done && !user_caps && c->n_nets <= 148 && c->max_in_agents < 32768 && c->max_in_vars < 16384) {
     Shape sh = base_shape(c, max_loops);
-    sh.res_vars = 16384;
-    sh.res_queue = 8192;
-    sh.ring_a = 16384;
-    sh.ring_v = 16384;
+    sh.res_vars = 14336;
+    sh.res_queue = 5120;
+    sh.ring_a = 8192;
+    sh.ring_v = 8192;
     int st = attempt_tier(kTierM, sh, 65535, sh.res_vars, 1);
     if (st == INET_OK && !any_oom()) done = true;
     else if (st != INET_OK && st != INET_ERR_UNSUPPORTED) return st;
@@ -487,7 +494,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
                                    cudaMemcpyDeviceToHost, c->stream));
     }
     if (c->count_rules) {
-      c->h_hist.resize(size_t(c->n_nets) * std::max(c->n_rules, 1u));
+      c->h_hist.resize(size_t(c->n_nets) * hist_stride(c));
       CUDA_TRY(cudaMemcpyAsync(c->h_hist.data(), c->d_hist.p, c->h_hist.size() * 4, cudaMemcpyDeviceToHost, c->stream));
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -542,8 +549,8 @@ int inet_batch_rule_counts(inet_ctx* c, uint32_t net, uint64_t* counts, uint32_t
   if (!c || !counts) return INET_ERR_ARG;
   if (!c->reduced || !c->count_rules || c->h_hist.empty()) return INET_ERR_STATE;
   if (net >= c->n_nets) return INET_ERR_ARG;
-  const uint32_t R = std::max(c->n_rules, 1u);
-  for (uint32_t r = 0; r < n_rules; ++r) counts[r] = r < c->n_rules ? c->h_hist[size_t(net) * R + r] : 0;
+  const uint32_t R = hist_stride(c);
+  for (uint32_t r = 0; r < n_rules; ++r) counts[r] = r < R ? c->h_hist[size_t(net) * R + r] : 0;
   return INET_OK;
 }
 
