@@ -249,7 +249,7 @@ def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
 
-    from paper_1404_0076_b200 import EngineConfig, _native, engine
+    from paper_1404_0076_b200 import EngineConfig, _native, engine, shard
     from paper_1404_0076_b200.programs import ackermann_value, fibonacci_value, program
 
     rank, local, world = dist_env()
@@ -260,7 +260,7 @@ def run_ours(args) -> None:
     name, params, wl = workload_spec(args.workload)
     prog = program(name)
     if args.workload == "batch":
-        lo, hi = rank * BATCH_NETS // world, (rank + 1) * BATCH_NETS // world
+        lo, hi = shard.shard_bounds(BATCH_NETS, world, rank)
         configs = [prog.build_input(*params) for _ in range(hi - lo)]
         per_net = GOLDEN_A36
     else:
@@ -307,11 +307,9 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
     my_ms = sum(times)
-    t = torch.tensor([my_ms], dtype=torch.float64, device=f"cuda:{dev}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    total_interactions = per_net * (BATCH_NETS if args.workload == "batch" else world)
+    max_ms = shard.max_over_ranks(my_ms, device=f"cuda:{dev}")
+    # interactions of one step, all ranks (each rank verified its own count above)
+    total_interactions = int(shard.sum_over_ranks([float(ti)], device=f"cuda:{dev}")[0])
     value = total_interactions * args.steps / (max_ms / 1000.0)
     kernel_ms = my_ms / args.steps
 
@@ -327,10 +325,8 @@ def run_ours(args) -> None:
         e2e_times.append(time.perf_counter() - t0)
         assert code == _native.OK and len(agents0) == height + 1
         h2d, d2h = ctx.io_bytes()
-    et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=f"cuda:{dev}")
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = total_interactions * len(e2e_times) / float(et.item())
+    e2e_max = shard.max_over_ranks(sum(e2e_times), device=f"cuda:{dev}")
+    e2e_value = total_interactions * len(e2e_times) / e2e_max
 
     peak, peak_kind = load_peaks()
     achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9

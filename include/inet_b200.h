@@ -42,8 +42,17 @@
 #ifndef INET_B200_H
 #define INET_B200_H
 
+#ifndef __CUDACC_RTC__
 #include <stddef.h>
 #include <stdint.h>
+#else
+typedef unsigned int uint32_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long size_t;
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -100,20 +109,35 @@ typedef struct inet_net_stats {
   uint32_t cap_agents;     /* capacities the successful run used */
   uint32_t cap_vars;
   uint32_t tier;           /* residency tier used: 0 S (shared), 1 M (mixed), 2 G (global) */
+  uint32_t jit;            /* 1 if the rule-set specialised kernel ran (else the interpreter) */
+  uint32_t reserved;
 } inet_net_stats;
 
-/* Context: one device, one stream, device buffers reused across calls. */
+/* Context: one device, one stream, device buffers reused across calls.
+ * Replaces the per-call ThreadPoolExecutor of evaluate (engine.py:201, 224-226). */
 int inet_ctx_create(int device, inet_ctx** out);
 void inet_ctx_destroy(inet_ctx* ctx);
 const char* inet_strerror(int status);
 /* Device properties for reporting: SM count and clock (kHz). */
 int inet_device_info(inet_ctx* ctx, int* sm_count, int* clock_khz, char* name, size_t name_len);
 
-/* Upload a compiled rule set (replaces RuleSet.lookup + instantiate tables). */
+/* Rule-set specialised kernels (NVRTC, compiled on first use and cached):
+ * mode 1 = use when available (default; env INET_B200_JIT=0 disables), 0 = the
+ * prebuilt table interpreter only. */
+int inet_set_jit(inet_ctx* ctx, int mode);
+/* Compile (or fetch from cache) the specialised kernel for a rule blob without
+ * a device; returns INET_OK or INET_ERR_UNSUPPORTED with the NVRTC log. */
+int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t threads, char* log, size_t log_len);
+
+/* Upload a compiled rule set. Replaces RuleSet.lookup / find_rule / instantiate
+ * (core.py:241-242, 281-312): the per-equation dictionary lookup and tree
+ * rebuild become one table lookup and a template expansion on the device. */
 int inet_rules_load(inet_ctx* ctx, const uint32_t* blob, size_t n_words);
 
 /*
- * Load a batch of nets (n_nets >= 1). Net i owns
+ * Load a batch of nets (n_nets >= 1). The Configuration argument of evaluate
+ * (engine.py:186-189; core.py:135-155) in flat form; n_nets == 1 is evaluate
+ * itself, n_nets > 1 is the new batch API. Net i owns
  *   agents[4*agent_off[i] .. 4*agent_off[i+1])   its agents (local indices)
  *   eqs[2*eq_off[i] .. 2*eq_off[i+1])             its equations
  *   iface[iface_off[i] .. iface_off[i+1])         its interface refs (host only)
@@ -125,7 +149,9 @@ int inet_batch_load(inet_ctx* ctx, uint32_t n_nets, const uint32_t* agents, cons
                     const uint64_t* iface_off, const uint32_t* n_vars);
 
 /*
- * Reduce every loaded net to its fixpoint on the device: the whole
+ * Reduce every loaded net to its fixpoint on the device (the loop of
+ * evaluate, engine.py:204-223: interaction_phase engine.py:106-134 and
+ * communication_phase + reduce_by_key engine.py:59-74, 137-166). The whole
  * interaction / communication loop runs inside one persistent kernel with no
  * host synchronisation per round (replaces engine.py:204-223). Host buffers
  * were copied by inet_batch_load; this call performs H2D, the kernel(s),
@@ -140,6 +166,8 @@ int inet_batch_reduce(inet_ctx* ctx, const inet_cfg* cfg, float* device_ms);
  * resident copy and run the kernel. For device-timed benchmarking. */
 int inet_batch_rerun(inet_ctx* ctx, const inet_cfg* cfg, float* device_ms);
 
+/* EvalResult.total_interactions / total_communications and the error of net i
+ * (engine.py:51-56; errors.py:46-56). */
 int inet_batch_stats(inet_ctx* ctx, uint32_t net, inet_net_stats* out);
 /* Interactions per rule of net i (needs cfg.count_rules); counts[n_rules]. */
 int inet_batch_rule_counts(inet_ctx* ctx, uint32_t net, uint64_t* counts, uint32_t n_rules);
@@ -149,19 +177,20 @@ int inet_batch_io_bytes(inet_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 int inet_batch_totals(inet_ctx* ctx, uint64_t* interactions, uint64_t* communications, uint32_t* max_rounds,
                       uint32_t* n_failed);
 
-/* Per-round rows of net i: 4 words per round {interactions, communications,
+/* EvalResult.loops (LoopStats rows, profile.py:16-22; engine.py:215-221).
+ * Per-round rows of net i: 4 words per round {interactions, communications,
  * live_equations, elapsed_ns}. Two-call protocol: rows==NULL returns count. */
 int inet_batch_rounds(inet_ctx* ctx, uint32_t net, uint32_t* rows, uint32_t* n_rows);
 
 /*
- * Sequential cleanup of net i (engine.py:287-362): splice every parked
+ * finalize (engine.py:287-362) of net i: splice every parked
  * equation into the other occurrence of its variable, in the reference's
  * queue order, then compact the reachable normal form. Runs on host threads
  * (all nets in parallel when net == INET_NONE).
  */
 int inet_batch_finalize(inet_ctx* ctx, uint32_t net, uint32_t n_threads);
 
-/* Normal form of net i after finalize: pointers stay valid until the next
+/* EvalResult.final (engine.py:227-228) of net i after finalize: pointers stay valid until the next
  * load/reduce/finalize on this context. Agents are in preorder (children
  * after parents), refs are local to these arrays; variable ids are the
  * device's (input ids 0..n_vars-1 are preserved, fresh ids >= n_vars). */
@@ -169,7 +198,7 @@ int inet_batch_result(inet_ctx* ctx, uint32_t net, const uint32_t** agents, uint
                       const uint32_t** iface, uint32_t* n_iface, const uint32_t** eqs, uint32_t* n_eqs);
 
 /*
- * Stand-alone finalize on caller buffers (engine.finalize's signature, flat):
+ * Stand-alone finalize on caller buffers (engine.finalize, engine.py:287, flat):
  * agents/iface/eqs are modified in place; alive[e] receives 1 for equations
  * that survive. n_vars bounds variable ids.
  */

@@ -26,6 +26,8 @@ EXPORTS = (
     "inet_strerror",
     "inet_device_info",
     "inet_rules_load",
+    "inet_set_jit",
+    "inet_jit_compile",
     "inet_batch_load",
     "inet_batch_reduce",
     "inet_batch_rerun",
@@ -67,6 +69,8 @@ class NetStats(C.Structure):
         ("cap_agents", C.c_uint32),
         ("cap_vars", C.c_uint32),
         ("tier", C.c_uint32),
+        ("jit", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -92,6 +96,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             "inet_strerror": (C.c_char_p, [C.c_int]),
             "inet_device_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
             "inet_rules_load": (C.c_int, [C.c_void_p, _u32p, C.c_size_t]),
+            "inet_set_jit": (C.c_int, [C.c_void_p, C.c_int]),
+            "inet_jit_compile": (C.c_int, [_u32p, C.c_size_t, C.c_int, C.c_uint32, C.c_char_p, C.c_size_t]),
             "inet_batch_load": (C.c_int, [C.c_void_p, C.c_uint32, _u32p, _u64p, _u32p, _u64p, _u32p, _u64p, _u32p]),
             "inet_batch_reduce": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
             "inet_batch_rerun": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
@@ -162,6 +168,10 @@ class Context:
         name = C.create_string_buffer(128)
         _check(self.lib.inet_device_info(self.h, C.byref(sms), C.byref(clk), name, 128), "device_info")
         return {"sm_count": sms.value, "clock_khz": clk.value, "name": name.value.decode()}
+
+    def set_jit(self, mode: bool) -> None:
+        """Rule-set specialised kernels on/off (default on when NVRTC is present)."""
+        _check(self.lib.inet_set_jit(self.h, 1 if mode else 0), "set_jit")
 
     def load_rules(self, blob: np.ndarray, key=None) -> None:
         if key is not None and key == self._blob_key:
@@ -264,6 +274,15 @@ def finalize_flat(agents: np.ndarray, iface: np.ndarray, eqs: np.ndarray, n_vars
     if code != OK:
         raise DeviceError(code, f"finalize_flat: {strerror(code)}")
     return agents, iface, eqs, alive[: len(eqs.reshape(-1)) // 2]
+
+
+def jit_compile(blob: np.ndarray, tier: int = 1, threads: int = 1024) -> tuple[int, str]:
+    """Compile the rule-set specialised kernel on the host (no device needed)."""
+    lib = load_library()
+    blob = np.ascontiguousarray(blob, dtype=np.uint32)
+    log = C.create_string_buffer(1 << 16)
+    code = lib.inet_jit_compile(_ptr(blob), blob.size, tier, threads, log, len(log))
+    return code, log.value.decode(errors="replace")
 
 
 _contexts: dict[int, Context] = {}

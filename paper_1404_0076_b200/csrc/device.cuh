@@ -41,7 +41,9 @@
 // bump pointer. Variable ids are recycled the same way once both occurrences
 // have met. A full ring drops the id (it is simply never reused).
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 #include "../../include/inet_b200.h"
 
@@ -348,6 +350,49 @@ __device__ __forceinline__ void link(Round<kTier>& c, uint32_t l, uint32_t r) {
   settle(c, x, atomicExch(&c.vslot[x], val), val);
 }
 
+#ifdef INET_JIT
+// Helpers of the generated rewrites: allocation with compile-time counts into
+// registers, and the first half of link() (push or exchange key).
+template <uint32_t N, int kTier>
+__device__ __forceinline__ bool jit_alloc_vars(Round<kTier>& c, uint32_t (&f)[N]) {
+  Claim k;
+  if (!alloc_vars(c, N, k)) return false;
+#pragma unroll
+  for (uint32_t j = 0; j < N; ++j)
+    f[j] = kVar | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : k.bump + (j - k.got));
+  return true;
+}
+
+template <uint32_t N, int kTier>
+__device__ __forceinline__ bool jit_alloc_agents(Round<kTier>& c, uint32_t (&g)[N]) {
+  Claim k;
+  if (!alloc_agents(c, N, k)) return false;
+#pragma unroll
+  for (uint32_t j = 0; j < N; ++j)
+    g[j] = j < k.got ? static_cast<uint32_t>(c.aring[(k.pos + j) & c.amask]) : k.bump + (j - k.got);
+  return true;
+}
+
+// Active pair -> queue (returns false); otherwise the slot key and the parked value.
+template <int kTier>
+__device__ __forceinline__ bool jit_prep(Round<kTier>& c, uint32_t l, uint32_t r, uint32_t& x, uint32_t& val) {
+  if (((l | r) & kVar) == 0) {
+    push_active(c, l, r);
+    return false;
+  }
+  uint32_t key;
+  key_of(l, r, key, val);
+  x = key & ~kVar;
+  return true;
+}
+
+// Rule-set specialised rewrite, generated per rule set by csrc/jit.cpp: one
+// straight-line case per rule with every source known at compile time.
+template <int kTier>
+__device__ __forceinline__ void jit_apply(Round<kTier>& c, uint32_t rule, const uint4& A, const uint4& B, uint32_t l,
+                                          uint32_t r);
+#endif
+
 // Rewrite one active pair (find_rule + instantiate, core.py:281-312).
 template <int kTier>
 __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r) {
@@ -369,6 +414,12 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
     r = u;
   }
   if (c.d->rule_hist) atomicAdd(&c.d->rule_hist[t >> 1], 1u);
+#ifdef INET_JIT
+  jit_apply<kTier>(c, t >> 1, A, B, l, r);
+  c.ints += 1;
+  INET_TMARK(c, 4);
+  return;
+#endif
   const uint32_t* R = c.rules + (t >> 1) * kRuleWords;
   const uint32_t hdr = R[0];
   const uint32_t nn = hdr & 0xFFu, ne = (hdr >> 8) & 0xFFu, nf = (hdr >> 16) & 0xFFu;
@@ -736,6 +787,25 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     if ((ahw > d.cap_agents || hw > d.cap_vars) && g->err == 0) g->err = INET_ERR_ARENA;
   }
   __syncthreads();
+}
+
+// Kernel body shared by the prebuilt kernels (engine.cu) and the rule-set
+// specialised ones (jit.cpp): load the rule table into shared memory, then
+// reduce the CTA's nets one after the other.
+template <int kBlock, int kTier>
+__device__ __forceinline__ void reduce_body(const NetDesc* __restrict__ nets, uint32_t n_nets,
+                                            const uint32_t* __restrict__ blob, const Shape& sh, uint32_t* smem,
+                                            NetDesc& sd) {
+  for (uint32_t i = threadIdx.x; i < sh.rule_words; i += kBlock) smem[i] = blob[4 + i];
+  const uint32_t pair_words = (sh.n_labels * sh.n_labels + 1) / 2;
+  const uint16_t* pair = reinterpret_cast<const uint16_t*>(smem);
+  const uint32_t* rules = smem + pair_words;
+  for (uint32_t net = blockIdx.x; net < n_nets; net += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) sd = nets[net];
+    __syncthreads();
+    run_net<kTier>(sd, sh, pair, rules, smem);
+  }
 }
 
 }  // namespace inetdev

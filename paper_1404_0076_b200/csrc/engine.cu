@@ -16,6 +16,11 @@
 #include "../../include/inet_b200.h"
 #include "device.cuh"
 #include "host.h"
+#include "jit.h"
+
+#include <cstdlib>
+#include <map>
+#include <tuple>
 
 using inetdev::NetCtl;
 using inetdev::NetDesc;
@@ -34,16 +39,7 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const NetDesc* __restric
                                                         const uint32_t* __restrict__ blob, Shape sh) {
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ NetDesc sd;
-  for (uint32_t i = threadIdx.x; i < sh.rule_words; i += kBlock) smem[i] = blob[4 + i];
-  const uint32_t pair_words = (sh.n_labels * sh.n_labels + 1) / 2;
-  const uint16_t* pair = reinterpret_cast<const uint16_t*>(smem);
-  const uint32_t* rules = smem + pair_words;
-  for (uint32_t net = blockIdx.x; net < n_nets; net += gridDim.x) {
-    __syncthreads();
-    if (threadIdx.x == 0) sd = nets[net];
-    __syncthreads();
-    inetdev::run_net<kTier>(sd, sh, pair, rules, smem);
-  }
+  inetdev::reduce_body<kBlock, kTier>(nets, n_nets, blob, sh, smem, sd);
 }
 
 using KernelFn = void (*)(const NetDesc*, uint32_t, const uint32_t*, Shape);
@@ -128,6 +124,11 @@ struct inet_ctx {
   std::vector<uint32_t> h_rounds;     // [n_nets * cap_rounds * 4]
   std::vector<inethost::NormalForm> results;
   std::vector<uint8_t> finalized;
+  // rule-set specialised kernels (jit.cpp), keyed by (tier, block size)
+  int jit_mode = 1;  // 0 = prebuilt interpreter only
+  bool last_jit = false;
+  std::string jit_log;
+  std::map<std::pair<int, uint32_t>, std::pair<cudaLibrary_t, cudaKernel_t>> jit_kernels;
 };
 
 inline uint32_t hist_stride(const inet_ctx* c) { return std::max(c->n_rules, 128u); }
@@ -177,6 +178,7 @@ int inet_ctx_create(int device, inet_ctx** out) {
   CUDA_TRY(cudaSetDevice(device));
   auto* c = new inet_ctx();
   c->device = device;
+  if (const char* e = std::getenv("INET_B200_JIT")) c->jit_mode = std::atoi(e);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
     delete c;
@@ -192,6 +194,7 @@ void inet_ctx_destroy(inet_ctx* c) {
   for (DevBuf* b : {&c->d_blob, &c->d_in_agents, &c->d_in_eqs, &c->d_desc, &c->d_agents, &c->d_vslot, &c->d_aring,
                     &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist})
     b->release();
+  for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -216,6 +219,10 @@ int inet_rules_load(inet_ctx* c, const uint32_t* blob, size_t n_words) {
   int st = inethost::validate_rule_blob(blob, n_words);
   if (st != INET_OK) return st;
   CUDA_TRY(cudaSetDevice(c->device));
+  if (c->blob.size() != n_words || !std::equal(c->blob.begin(), c->blob.end(), blob)) {
+    for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
+    c->jit_kernels.clear();
+  }
   c->blob.assign(blob, blob + n_words);
   c->n_labels = blob[1];
   c->n_rules = blob[2];
@@ -326,25 +333,56 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
 }
 
 // One attempt at the current capacities and tier: one kernel launch, timed.
+// Rule-set specialised kernel for (tier, threads), compiled on first use;
+// nullptr when NVRTC is unavailable or compilation failed (then the prebuilt
+// interpreter runs).
+const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
+  if (!c->jit_mode) return nullptr;
+  const auto key = std::make_pair(tier, threads);
+  auto it = c->jit_kernels.find(key);
+  if (it != c->jit_kernels.end()) return reinterpret_cast<const void*>(it->second.second);
+  const std::string src = inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads);
+  std::vector<char> cubin;
+  if (inetjit::compile_cubin(src, cubin, c->jit_log) != 0) {
+    std::fprintf(stderr, "inet_b200: rule-set JIT unavailable, using the prebuilt kernels: %s\n", c->jit_log.c_str());
+    c->jit_mode = 0;
+    return nullptr;
+  }
+  cudaLibrary_t lib;
+  cudaKernel_t k;
+  if (cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+      cudaLibraryGetKernel(&k, lib, "inet_jit_kernel") != cudaSuccess) {
+    cudaGetLastError();
+    std::fprintf(stderr, "inet_b200: could not load the JIT cubin, using the prebuilt kernels\n");
+    c->jit_mode = 0;
+    return nullptr;
+  }
+  c->jit_kernels[key] = {lib, k};
+  return reinterpret_cast<const void*>(k);
+}
+
 int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
   const uint32_t threads = auto_threads(c, cfg);
   sh.threads = threads;
-  KernelFn fn = pick_kernel(threads, tier);
+  const void* jk = jit_kernel(c, tier, threads);
+  const void* fn = jk ? jk : reinterpret_cast<const void*>(pick_kernel(threads, tier));
+  c->last_jit = jk != nullptr;
   const size_t smem = size_t(plan_smem(sh, tier).words) * 4;
   int dev_sms = 0, max_optin = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
   if (smem + sizeof(NetDesc) > size_t(max_optin)) return INET_ERR_UNSUPPORTED;
-  CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), smem);
   uint32_t grid = std::max(1, dev_sms * std::max(per_sm, 1));
   grid = std::min(grid, c->n_nets);
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-  fn<<<grid, threads, smem, c->stream>>>(static_cast<const NetDesc*>(c->d_desc.p), c->n_nets,
-                                         static_cast<const uint32_t*>(c->d_blob.p), sh);
-  CUDA_TRY(cudaGetLastError());
+  const NetDesc* a_nets = static_cast<const NetDesc*>(c->d_desc.p);
+  uint32_t a_n = c->n_nets;
+  const uint32_t* a_blob = static_cast<const uint32_t*>(c->d_blob.p);
+  void* args[] = {&a_nets, &a_n, &a_blob, &sh};
+  CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, c->stream));
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
   CUDA_TRY(cudaEventSynchronize(c->ev1));
   CUDA_TRY(cudaEventElapsedTime(ms, c->ev0, c->ev1));
@@ -460,6 +498,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     s.cap_agents = c->cap_agents;
     s.cap_vars = c->cap_vars;
     s.tier = static_cast<uint32_t>(c->tier);
+    s.jit = c->last_jit ? 1u : 0u;
     if (first == INET_OK && k.err) first = static_cast<int>(k.err);
   }
   c->reduced = true;
@@ -542,6 +581,25 @@ int inet_batch_stats(inet_ctx* c, uint32_t net, inet_net_stats* out) {
   if (!c->reduced) return INET_ERR_STATE;
   if (net >= c->n_nets) return INET_ERR_ARG;
   *out = c->stats[net];
+  return INET_OK;
+}
+
+int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t threads, char* log, size_t log_len) {
+  if (!blob || n_words < 4) return INET_ERR_ARG;
+  if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
+  std::vector<char> cubin;
+  std::string msg;
+  const int rc = inetjit::compile_cubin(inetjit::kernel_source(blob, n_words, tier, threads), cubin, msg);
+  if (log && log_len) {
+    std::strncpy(log, msg.c_str(), log_len - 1);
+    log[log_len - 1] = 0;
+  }
+  return rc == 0 ? INET_OK : INET_ERR_UNSUPPORTED;
+}
+
+int inet_set_jit(inet_ctx* c, int mode) {
+  if (!c) return INET_ERR_ARG;
+  c->jit_mode = mode ? 1 : 0;
   return INET_OK;
 }
 

@@ -1,0 +1,19 @@
+// jit.h — rule-set specialised kernels (see jit.cpp).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace inetjit {
+
+// CUDA source of the per-rule rewrites (jit_apply) for a rule blob.
+std::string generate_rules(const uint32_t* blob, size_t n_words);
+// Complete translation unit: device code + rewrites + one kernel `inet_jit_kernel`.
+std::string kernel_source(const uint32_t* blob, size_t n_words, int tier, uint32_t block);
+// NVRTC loadable?
+bool available();
+// Compile (or fetch from the on-disk cache) to an sm_100a cubin; 0 on success.
+int compile_cubin(const std::string& source, std::vector<char>& cubin, std::string& log);
+
+}  // namespace inetjit
