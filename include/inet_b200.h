@@ -110,7 +110,7 @@ typedef struct inet_net_stats {
   uint32_t cap_vars;
   uint32_t tier;           /* residency tier used: 0 S (shared), 1 M (mixed), 2 G (global) */
   uint32_t jit;            /* 1 if the rule-set specialised kernel ran (else the interpreter) */
-  uint32_t reserved;
+  uint32_t sm_mhz;         /* effective SM clock over this net's reduction (clock64 / globaltimer) */
 } inet_net_stats;
 
 /* Context: one device, one stream, device buffers reused across calls.

@@ -70,7 +70,7 @@ class NetStats(C.Structure):
         ("cap_vars", C.c_uint32),
         ("tier", C.c_uint32),
         ("jit", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("sm_mhz", C.c_uint32),
     ]
 
 

@@ -58,7 +58,7 @@ constexpr int kEnvSize = 23;  // sources 0..22 (22 = none)
 constexpr int kRuleWords = 16;
 constexpr int kFastEq = 4;  // rhs equations linked with overlapped exchanges
 
-enum : int { kTierS = 0, kTierM = 1, kTierG = 2 };
+enum : int { kTierS = 0, kTierM = 1, kTierG = 2, kTierC = 3 };
 
 template <int kTier>
 struct Traits {
@@ -78,19 +78,25 @@ struct Traits<kTierG> {
   static constexpr bool kSlotsSmem = false;
   static constexpr bool kPacked = false;
 };
+// Tier C: one net on a thread-block cluster; agents, slots and queues in
+// global memory (L2-resident), rings and round counters per CTA.
+template <>
+struct Traits<kTierC> : Traits<kTierG> {};
 
 // Counters of the running round, bumped by every thread while it works.
+// (Tier C reads {qcount, ints, comms, parked} of every CTA with one 16-byte
+// distributed-shared-memory load, so they lead.)
+constexpr uint32_t kErrBit = 0x80000000u;  // in qcount: a failure in this round
 struct RoundCtr {
-  uint32_t qcount;  // active pairs queued for the next round
+  uint32_t qcount;  // active pairs queued for the next round (| kErrBit on failure)
+  uint32_t ints;
+  uint32_t comms;
+  int32_t parked;   // delta of parked equations
   uint32_t atake;   // agent ring entries taken
   uint32_t afree;   // agents offered to the ring
   uint32_t vtake;
   uint32_t vfree;
-  uint32_t ints;
-  uint32_t comms;
-  int32_t parked;   // delta of parked equations
-  uint32_t err;     // any failure in this round
-  uint32_t pad[3];
+  uint32_t pad[4];
 };
 
 // Parameters of the next round, written by the last warp to finish a round
@@ -117,6 +123,7 @@ struct Ctl {
   unsigned long long t_prev;
   unsigned long long tot_i;
   unsigned long long tot_c;
+  uint32_t fpos_a, fpos_v;  // tier C: ring positions handed to freers (monotonic)
   uint32_t scratch[34];
 };
 
@@ -132,8 +139,17 @@ struct NetCtl {
   uint32_t parked_total;
   unsigned long long interactions;
   unsigned long long communications;
-  uint32_t pad[4];
+  uint32_t pad[4];  // pad[0]: effective SM clock (MHz) over the reduction
 };
+
+// Effective SM clock between two (clock64, globaltimer) samples, in MHz.
+__device__ __forceinline__ uint32_t clock_mhz(long long c0, unsigned long long g0) {
+  const long long dc = clock64() - c0;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned long long dg = t - g0;
+  return dg ? static_cast<uint32_t>(static_cast<unsigned long long>(dc) * 1000ull / dg) : 0u;
+}
 
 // Per-net device view of its private global arrays.
 struct NetDesc {
@@ -184,6 +200,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   } while (0)
 #endif
 
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane, uint32_t& total) {
+  uint32_t inc = v;
+#pragma unroll
+  for (uint32_t o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+  return inc - v;
+}
+
 template <class T>
 __device__ __forceinline__ T vload(const T* p) {
   return *reinterpret_cast<const volatile T*>(p);
@@ -208,6 +235,8 @@ struct Round {
   uint32_t cap_agents, cap_vars, cap_queue;
   uint32_t amask, vmask;
   uint32_t lo_a, hi_a, lo_v, hi_v;  // ring windows available this round
+  uint32_t a_base, v_base, stride;  // tier C: bump sequence s -> id base + stride * s
+  uint32_t rank, gshift;            // tier C: this CTA's rank in the cluster, log2 G
   uint32_t ints, comms;
   int32_t parked;
   bool failed;
@@ -215,12 +244,24 @@ struct Round {
   long long tm[8];
   long long tlast;
 #endif
+#ifdef INET_TRACE
+  long long tr[8];
+#endif
 };
+
+#ifdef INET_TRACE
+__device__ unsigned int inet_trace_count;
+#define INET_TR(c, k) ((c).tr[k] = clock64())
+#else
+#define INET_TR(c, k) \
+  do {                \
+  } while (0)
+#endif
 
 template <int kTier>
 __device__ __forceinline__ void fail(Round<kTier>& c, uint32_t code, uint32_t a = 0, uint32_t b = 0) {
   c.failed = true;
-  c.cur->err = 1u;
+  atomicOr(&c.cur->qcount, kErrBit);
   if (atomicCAS(&c.ctl->err_code, 0u, code) == 0u) {
     c.ctl->err_a = a;
     c.ctl->err_b = b;
@@ -232,6 +273,112 @@ __device__ __forceinline__ void fail(Round<kTier>& c, uint32_t code, uint32_t a 
 struct Claim {
   uint32_t pos, got, bump;
 };
+
+// Id of the s-th bump allocation. Tier C interleaves the CTAs of a cluster
+// (CTA k owns base + k + G*s), so ids stay dense without a shared counter.
+template <int kTier>
+__device__ __forceinline__ uint32_t bump_agent(const Round<kTier>& c, uint32_t s) {
+  if constexpr (kTier == kTierC) return c.a_base + c.stride * s;
+  else return s;
+}
+template <int kTier>
+__device__ __forceinline__ uint32_t bump_var(const Round<kTier>& c, uint32_t s) {
+  if constexpr (kTier == kTierC) return c.v_base + c.stride * s;
+  else return s;
+}
+
+
+// ---- thread-block-cluster primitives (tier C) ------------------------------
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ uint32_t dsmem_atom_add(const void* p, uint32_t rank, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(dsmem_addr(p, rank)), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void dsmem_red_add(const void* p, uint32_t rank, uint32_t v) {
+  asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(dsmem_addr(p, rank)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st(const void* p, uint32_t rank, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(dsmem_addr(p, rank)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st4(const void* p, uint32_t rank, uint4 v) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dsmem_addr(p, rank)), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_ld(const void* p, uint32_t rank) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+
+// Tier C free: an id goes back to the ring of the CTA that owns it
+// (owner = id mod G), at a position drawn from the owner's monotonic counter;
+// the owner's per-round count makes it allocatable from the next round on.
+// A CTA never owns more ids than its ring holds, so nothing is dropped.
+template <int kTier>
+__device__ __forceinline__ void free_owned(Round<kTier>& c, uint32_t id, uint32_t* fpos, uint32_t* ring, uint32_t mask,
+                                           uint32_t* cnt) {
+  const uint32_t k = id & (c.stride - 1);
+  if (k == c.rank) {
+    const uint32_t pos = atomicAdd(fpos, 1u);
+    ring[pos & mask] = id;
+    atomicAdd(cnt, 1u);
+  } else {
+    const uint32_t pos = dsmem_atom_add(fpos, k, 1u);
+    dsmem_st(&ring[pos & mask], k, id);
+    dsmem_red_add(cnt, k, 1u);
+  }
+}
+
+
+// ---- agent and variable-slot access -----------------------------------------
+// Tiers S/M/G address one array; tier C spreads both over the cluster's shared
+// memory (id -> CTA id & (G-1), slot id >> log2 G).
+__device__ __forceinline__ uint4 dsmem_ld4(const void* p, uint32_t rank) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(dsmem_addr(p, rank))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 dsmem_ld2(const void* p, uint32_t rank) {
+  uint2 v;
+  asm volatile("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t dsmem_exch(const void* p, uint32_t rank, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cluster.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(dsmem_addr(p, rank)), "r"(v) : "memory");
+  return old;
+}
+
+template <int kTier>
+__device__ __forceinline__ uint4 ld_agent(const Round<kTier>& c, uint32_t a) {
+  if constexpr (kTier == kTierC) return dsmem_ld4(c.agents + (a >> c.gshift), a & (c.stride - 1));
+  else return c.agents[a];
+}
+template <int kTier>
+__device__ __forceinline__ void st_agent(const Round<kTier>& c, uint32_t a, const uint4& v) {
+  if constexpr (kTier == kTierC) dsmem_st4(c.agents + (a >> c.gshift), a & (c.stride - 1), v);
+  else c.agents[a] = v;
+}
+template <int kTier>
+__device__ __forceinline__ uint32_t exch_slot(const Round<kTier>& c, uint32_t x, uint32_t v) {
+  if constexpr (kTier == kTierC) return dsmem_exch(c.vslot + (x >> c.gshift), x & (c.stride - 1), v);
+  else return atomicExch(&c.vslot[x], v);
+}
+template <int kTier>
+__device__ __forceinline__ void st_slot(const Round<kTier>& c, uint32_t x, uint32_t v) {
+  if constexpr (kTier == kTierC) dsmem_st(c.vslot + (x >> c.gshift), x & (c.stride - 1), v);
+  else c.vslot[x] = v;
+}
 
 template <int kTier>
 __device__ __forceinline__ bool alloc_vars(Round<kTier>& c, uint32_t nf, Claim& k) {
@@ -273,6 +420,10 @@ __device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, Claim&
 
 template <int kTier>
 __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
+  if constexpr (kTier == kTierC) {
+    free_owned(c, a, &c.ctl->fpos_a, reinterpret_cast<uint32_t*>(c.aring), c.amask, &c.cur->afree);
+    return;
+  }
   const uint32_t f = atomicAdd(&c.cur->afree, 1u);
   const uint32_t pos = c.hi_a + f;
   if (pos - c.lo_a <= c.amask) c.aring[pos & c.amask] = a;  // else dropped
@@ -280,11 +431,16 @@ __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
 
 template <int kTier>
 __device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
+  if constexpr (kTier == kTierC) {
+    free_owned(c, x, &c.ctl->fpos_v, reinterpret_cast<uint32_t*>(c.vring), c.vmask, &c.cur->vfree);
+    return;
+  }
   const uint32_t f = atomicAdd(&c.cur->vfree, 1u);
   const uint32_t pos = c.hi_v + f;
   if (pos - c.lo_v <= c.vmask) c.vring[pos & c.vmask] = x;
 }
 
+// Queue an active pair.
 template <int kTier>
 __device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_t r) {
   const uint32_t p = atomicAdd(&c.cur->qcount, 1u);
@@ -294,6 +450,27 @@ __device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_
   }
   if constexpr (Traits<kTier>::kPacked)
     static_cast<uint32_t*>(c.out)[p] = (l << 16) | r;  // both < 65536 in tiers S/M
+  else
+    static_cast<uint2*>(c.out)[p] = make_uint2(l, r);
+}
+
+// Warp-collective push: every lane calls it, lanes with `pu` push (l, r).
+template <int kTier>
+__device__ __forceinline__ void warp_push(Round<kTier>& c, bool pu, uint32_t l, uint32_t r) {
+  const uint32_t m = __ballot_sync(0xFFFFFFFFu, pu);
+  if (!m) return;
+  const uint32_t lane = threadIdx.x & 31u, leader = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(&c.cur->qcount, static_cast<uint32_t>(__popc(m)));
+  base = __shfl_sync(0xFFFFFFFFu, base, leader);
+  if (!pu) return;
+  const uint32_t p = base + __popc(m & ((1u << lane) - 1u));
+  if (p >= c.cap_queue) {
+    fail(c, INET_ERR_ARENA, 2);
+    return;
+  }
+  if constexpr (Traits<kTier>::kPacked)
+    static_cast<uint32_t*>(c.out)[p] = (l << 16) | r;
   else
     static_cast<uint2*>(c.out)[p] = make_uint2(l, r);
 }
@@ -322,7 +499,7 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
       c.parked += 1;
       return;
     }
-    c.vslot[x] = kNone;  // x is dead: both occurrences met
+    st_slot(c, x, kNone);  // x is dead: both occurrences met
     c.comms += 1;
     c.parked -= 1;
     free_var(c, x);
@@ -334,7 +511,7 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
     uint32_t key;
     key_of(l, r, key, val);
     x = key & ~kVar;
-    old = atomicExch(&c.vslot[x], val);
+    old = exch_slot(c, x, val);
   }
 }
 
@@ -347,7 +524,7 @@ __device__ __forceinline__ void link(Round<kTier>& c, uint32_t l, uint32_t r) {
   uint32_t key, val;
   key_of(l, r, key, val);
   const uint32_t x = key & ~kVar;
-  settle(c, x, atomicExch(&c.vslot[x], val), val);
+  settle(c, x, exch_slot(c, x, val), val);
 }
 
 #ifdef INET_JIT
@@ -359,7 +536,7 @@ __device__ __forceinline__ bool jit_alloc_vars(Round<kTier>& c, uint32_t (&f)[N]
   if (!alloc_vars(c, N, k)) return false;
 #pragma unroll
   for (uint32_t j = 0; j < N; ++j)
-    f[j] = kVar | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : k.bump + (j - k.got));
+    f[j] = kVar | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
   return true;
 }
 
@@ -369,9 +546,97 @@ __device__ __forceinline__ bool jit_alloc_agents(Round<kTier>& c, uint32_t (&g)[
   if (!alloc_agents(c, N, k)) return false;
 #pragma unroll
   for (uint32_t j = 0; j < N; ++j)
-    g[j] = j < k.got ? static_cast<uint32_t>(c.aring[(k.pos + j) & c.amask]) : k.bump + (j - k.got);
+    g[j] = j < k.got ? static_cast<uint32_t>(c.aring[(k.pos + j) & c.amask]) : bump_agent(c, k.bump + (j - k.got));
   return true;
 }
+
+// Runtime counts (n <= N): ids land in f[0..n), the rest are untouched.
+template <uint32_t N, int kTier>
+__device__ __forceinline__ bool jit_alloc_vars_n(Round<kTier>& c, uint32_t n, uint32_t (&f)[N]) {
+  Claim k;
+  if (!alloc_vars(c, n, k)) return false;
+#pragma unroll
+  for (uint32_t j = 0; j < N; ++j)
+    if (j < n)
+      f[j] = kVar | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
+  return true;
+}
+
+template <uint32_t N, int kTier>
+__device__ __forceinline__ bool jit_alloc_agents_n(Round<kTier>& c, uint32_t n, uint32_t (&g)[N]) {
+  Claim k;
+  if (!alloc_agents(c, n, k)) return false;
+#pragma unroll
+  for (uint32_t j = 0; j < N; ++j)
+    if (j < n)
+      g[j] = j < k.got ? static_cast<uint32_t>(c.aring[(k.pos + j) & c.amask]) : bump_agent(c, k.bump + (j - k.got));
+  return true;
+}
+
+// Warp-collective allocation for the rule-set kernels: every lane asks for nf
+// fresh variables and nx extra agents; one lane claims the warp's total on
+// each ring (two independent atomics), overflow goes to the bump pointers.
+// Returns false on every lane if an arena is exhausted.
+template <uint32_t MF, uint32_t MX, int kTier>
+__device__ __forceinline__ bool jit_warp_alloc(Round<kTier>& c, uint32_t nf, uint32_t nx, uint32_t (&f)[MF],
+                                               uint32_t (&g)[MX]) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t tot_f, tot_x;
+  const uint32_t ex_f = warp_excl_scan(nf, lane, tot_f);
+  const uint32_t ex_x = warp_excl_scan(nx, lane, tot_x);
+  if ((tot_f | tot_x) == 0) return true;
+  const uint32_t av_v = c.hi_v - c.lo_v, av_a = c.hi_a - c.lo_a;
+  uint32_t tv = 0, ta = 0, bv = 0, ba = 0, ok = 1;
+  if (lane == 0) {
+    if (tot_f) tv = atomicAdd(&c.cur->vtake, tot_f);
+    if (tot_x) ta = atomicAdd(&c.cur->atake, tot_x);
+    const uint32_t ov = tv + tot_f > av_v ? tv + tot_f - max(tv, av_v) : 0u;
+    const uint32_t oa = ta + tot_x > av_a ? ta + tot_x - max(ta, av_a) : 0u;
+    if (ov) {
+      bv = atomicAdd(&c.ctl->var_bump, ov);
+      if (bv + ov > c.cap_vars) {
+        fail(c, INET_ERR_ARENA, 1);
+        ok = 0;
+      }
+    }
+    if (oa) {
+      ba = atomicAdd(&c.ctl->agent_bump, oa);
+      if (ba + oa > c.cap_agents) {
+        fail(c, INET_ERR_ARENA, 0);
+        ok = 0;
+      }
+    }
+  }
+  if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) {
+    c.failed = true;
+    return false;
+  }
+  tv = __shfl_sync(0xFFFFFFFFu, tv, 0);
+  ta = __shfl_sync(0xFFFFFFFFu, ta, 0);
+  bv = __shfl_sync(0xFFFFFFFFu, bv, 0);
+  ba = __shfl_sync(0xFFFFFFFFu, ba, 0);
+  const uint32_t fb_v = max(tv, av_v), fb_a = max(ta, av_a);  // first bumped take index
+#pragma unroll
+  for (uint32_t j = 0; j < MF; ++j)
+    if (j < nf) {
+      const uint32_t q = tv + ex_f + j;
+      f[j] = kVar | (q < av_v ? static_cast<uint32_t>(c.vring[(c.lo_v + q) & c.vmask]) : bump_var(c, bv + (q - fb_v)));
+    }
+#pragma unroll
+  for (uint32_t j = 0; j < MX; ++j)
+    if (j < nx) {
+      const uint32_t q = ta + ex_x + j;
+      g[j] = q < av_a ? static_cast<uint32_t>(c.aring[(c.lo_a + q) & c.amask]) : bump_agent(c, ba + (q - fb_a));
+    }
+  return true;
+}
+
+// Rule-set specialised rewrites, generated per rule set by csrc/jit.cpp.
+template <int kTier>
+__device__ __forceinline__ void jit_warp(Round<kTier>& c, bool valid, uint32_t l, uint32_t r);
+template <int kTier>
+__device__ __forceinline__ void jit_apply(Round<kTier>& c, uint32_t rule, const uint4& A, const uint4& B, uint32_t l,
+                                          uint32_t r);
 
 // Active pair -> queue (returns false); otherwise the slot key and the parked value.
 template <int kTier>
@@ -386,21 +651,18 @@ __device__ __forceinline__ bool jit_prep(Round<kTier>& c, uint32_t l, uint32_t r
   return true;
 }
 
-// Rule-set specialised rewrite, generated per rule set by csrc/jit.cpp: one
-// straight-line case per rule with every source known at compile time.
-template <int kTier>
-__device__ __forceinline__ void jit_apply(Round<kTier>& c, uint32_t rule, const uint4& A, const uint4& B, uint32_t l,
-                                          uint32_t r);
 #endif
 
 // Rewrite one active pair (find_rule + instantiate, core.py:281-312).
 template <int kTier>
 __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r) {
   INET_TMARK(c, 0);
-  uint4 A = c.agents[l];
-  uint4 B = c.agents[r];
+  INET_TR(c, 1);
+  uint4 A = ld_agent(c, l);
+  uint4 B = ld_agent(c, r);
   const uint32_t t = c.pair[A.x * c.n_labels + B.x];
   INET_TMARK(c, 1);
+  INET_TR(c, 2);
   if (t == 0xFFFFu) {
     fail(c, INET_ERR_NO_RULE, A.x, B.x);
     return;
@@ -413,7 +675,9 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
     l = r;
     r = u;
   }
+#ifndef INET_CTIMING
   if (c.d->rule_hist) atomicAdd(&c.d->rule_hist[t >> 1], 1u);
+#endif
 #ifdef INET_JIT
   jit_apply<kTier>(c, t >> 1, A, B, l, r);
   c.ints += 1;
@@ -427,11 +691,12 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
   if (!alloc_vars(c, nf, fv)) return;
   if (!alloc_agents(c, nn > 2 ? nn - 2 : 0, na)) return;
   INET_TMARK(c, 2);
+  INET_TR(c, 3);
   auto fresh = [&](uint32_t j) -> uint32_t {
-    return kVar | (j < fv.got ? static_cast<uint32_t>(c.vring[(fv.pos + j) & c.vmask]) : fv.bump + (j - fv.got));
+    return kVar | (j < fv.got ? static_cast<uint32_t>(c.vring[(fv.pos + j) & c.vmask]) : bump_var(c, fv.bump + (j - fv.got)));
   };
   auto extra = [&](uint32_t q) -> uint32_t {
-    return q < na.got ? static_cast<uint32_t>(c.aring[(na.pos + q) & c.amask]) : na.bump + (q - na.got);
+    return q < na.got ? static_cast<uint32_t>(c.aring[(na.pos + q) & c.amask]) : bump_agent(c, na.bump + (q - na.got));
   };
   uint32_t env_l[Traits<kTier>::kEnvLocal ? kEnvSize : 1];
   if constexpr (Traits<kTier>::kEnvLocal) {
@@ -485,11 +750,12 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
   };
   for (uint32_t m = 0; m < nn; ++m) {
     const uint32_t w = R[1 + m];
-    c.agents[src(kEnvNew + m)] = make_uint4(w & 0xFFu, src((w >> 8) & 0xFFu), src((w >> 16) & 0xFFu), src(w >> 24));
+    st_agent(c, src(kEnvNew + m), make_uint4(w & 0xFFu, src((w >> 8) & 0xFFu), src((w >> 16) & 0xFFu), src(w >> 24)));
   }
   if (nn < 2) free_agent(c, r);
   if (nn < 1) free_agent(c, l);
   INET_TMARK(c, 3);
+  INET_TR(c, 4);
   // Link the rhs: issue the first exchange of every equation back to back so
   // their latencies overlap, then settle each.
   uint32_t xs[kFastEq], olds[kFastEq], vals[kFastEq];
@@ -505,10 +771,11 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
         uint32_t key;
         key_of(el, er, key, vals[e]);
         xs[e] = key & ~kVar;
-        olds[e] = atomicExch(&c.vslot[xs[e]], vals[e]);
+        olds[e] = exch_slot(c, xs[e], vals[e]);
       }
     }
   }
+  INET_TR(c, 5);
 #pragma unroll
   for (int e = 0; e < kFastEq; ++e)
     if (xs[e] != kNone) settle(c, xs[e], olds[e], vals[e]);
@@ -518,6 +785,24 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
   }
   c.ints += 1;
   INET_TMARK(c, 4);
+}
+
+#ifdef INET_JIT_WARP
+constexpr bool kWarpRewrite = true;
+#else
+constexpr bool kWarpRewrite = false;
+#endif
+
+// Warp-collective entry: every lane of the warp calls it; lanes with `valid`
+// rewrite their pair. The rule-set kernels run the whole warp through one
+// specialised rewrite (jit_warp); the interpreter handles lanes one by one.
+template <int kTier>
+__device__ __forceinline__ void interact_w(Round<kTier>& c, bool valid, uint32_t l, uint32_t r) {
+#ifdef INET_JIT_WARP
+  jit_warp<kTier>(c, valid, l, r);
+#else
+  if (valid) interact(c, l, r);
+#endif
 }
 
 // Block-wide exclusive prefix of a 0/1 flag; returns the total.
@@ -547,22 +832,32 @@ __device__ __forceinline__ uint32_t block_scan_flag(bool flag, uint32_t* warp_to
 // Shared-memory plan (32-bit words):
 //   rule table | Ctl | agent ring | var ring | [S: agents] | [S,M: slots] | [S,M: 2 queues]
 struct SmemPlan {
-  uint32_t ctl_off, aring_off, vring_off, agents_off, slots_off, queue_off, env_off, words;
+  uint32_t ctl_off, aring_off, vring_off, agents_off, slots_off, queue_off, env_off, cagent_off, words;
 };
 
 __host__ __device__ inline uint32_t align4(uint32_t w) { return (w + 3u) & ~3u; }
 
+// Shared-memory plan (32-bit words):
+//   S: rules | Ctl | u16 rings | agents | slots | 2 packed queues
+//   M: rules | Ctl | u16 rings | slots | 2 packed queues        (agents global)
+//   G: rules | Ctl | u32 rings                                   (rest global)
+//   C: rules | Ctl | u32 rings | 3 counter sets + inbox | slots | 2 queues | agents
+//      (this CTA's share of the cluster-wide arrays)
 __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
-  const uint32_t ring_bytes = tier == kTierG ? 4u : 2u;
+  const uint32_t ring_bytes = tier >= kTierG ? 4u : 2u;
   SmemPlan p;
   p.ctl_off = align4(sh.rule_words);
   p.aring_off = p.ctl_off + align4(sizeof(Ctl) / 4);
   p.vring_off = p.aring_off + align4((sh.ring_a * ring_bytes + 3) / 4);
   p.agents_off = p.vring_off + align4((sh.ring_v * ring_bytes + 3) / 4);
-  p.slots_off = p.agents_off + (tier == kTierS ? 4 * sh.res_agents : 0);
-  p.queue_off = p.slots_off + (tier != kTierG ? align4(sh.res_vars) : 0);
-  p.env_off = p.queue_off + (tier != kTierG ? align4(2 * sh.res_queue) : 0);
-  p.words = p.env_off;  // (shared source table disabled: measured slower than registers)
+  p.slots_off = p.agents_off + (tier == kTierS ? 4 * sh.res_agents
+                                : tier == kTierC ? align4(3 * sizeof(RoundCtr) / 4 + 3 * 16 * 4) : 0);
+  const bool res_slots = tier != kTierG;
+  p.queue_off = p.slots_off + (res_slots ? align4(sh.res_vars) : 0);
+  const uint32_t qwords = tier == kTierC ? 2 * 2 * sh.res_queue : 2 * sh.res_queue;  // C: uint2 entries
+  p.env_off = p.queue_off + (res_slots ? align4(qwords) : 0);
+  p.cagent_off = p.env_off;
+  p.words = p.cagent_off + (tier == kTierC ? 4 * sh.res_agents : 0);
   return p;
 }
 
@@ -606,6 +901,8 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   }
   if constexpr (T::kPacked) c.cap_agents = min(c.cap_agents, 65535u);
   qstride = c.cap_queue;
+  const long long clk0 = clock64();
+  const unsigned long long gt0 = globaltimer();
   // ---- init: private copy of the input agents, empty slots, zero counters
   const bool fits = d.n_in_agents <= c.cap_agents && d.n_in_vars <= c.cap_vars;
   for (uint32_t i = threadIdx.x; i < c.cap_vars; i += blockDim.x) c.vslot[i] = kNone;
@@ -658,26 +955,55 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       // the input equations, in any class (communication_phase's first pass)
       c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + qstride)
                          : static_cast<void*>(static_cast<uint2*>(q0) + qstride);
-      for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
-        const uint2 eq = d.in_eqs[i];
-        if (((eq.x | eq.y) & kVar) == 0)
-          interact(c, eq.x, eq.y);
-        else
-          link(c, eq.x, eq.y);
+      if constexpr (kWarpRewrite) {
+        for (uint32_t b = threadIdx.x & ~31u; b < n; b += blockDim.x) {
+          const uint32_t i = b + lane;
+          const bool v = i < n && !c.failed;
+          const uint2 eq = v ? d.in_eqs[i] : make_uint2(0, 0);
+          const bool act = v && ((eq.x | eq.y) & kVar) == 0;
+          interact_w(c, act, eq.x, eq.y);
+          if (v && !act && !c.failed) link(c, eq.x, eq.y);
+        }
+      } else {
+        for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
+          const uint2 eq = d.in_eqs[i];
+          if (((eq.x | eq.y) & kVar) == 0)
+            interact(c, eq.x, eq.y);
+          else
+            link(c, eq.x, eq.y);
+        }
       }
     } else if constexpr (T::kPacked) {
       const uint32_t* in = static_cast<const uint32_t*>(q0) + ((r - 1) & 1u) * qstride;
       c.out = static_cast<uint32_t*>(q0) + (r & 1u) * qstride;
-      for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
-        const uint32_t w = in[i];
-        interact(c, w >> 16, w & 0xFFFFu);
+      if constexpr (kWarpRewrite) {
+        for (uint32_t b = threadIdx.x & ~31u; b < n; b += blockDim.x) {
+          const uint32_t i = b + lane;
+          const bool v = i < n && !c.failed;
+          const uint32_t w = v ? in[i] : 0u;
+          interact_w(c, v, w >> 16, w & 0xFFFFu);
+        }
+      } else {
+        for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
+          const uint32_t w = in[i];
+          interact(c, w >> 16, w & 0xFFFFu);
+        }
       }
     } else {
       const uint2* in = static_cast<const uint2*>(q0) + ((r - 1) & 1u) * qstride;
       c.out = static_cast<uint2*>(q0) + (r & 1u) * qstride;
-      for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
-        const uint2 eq = in[i];
-        interact(c, eq.x, eq.y);
+      if constexpr (kWarpRewrite) {
+        for (uint32_t b = threadIdx.x & ~31u; b < n; b += blockDim.x) {
+          const uint32_t i = b + lane;
+          const bool v = i < n && !c.failed;
+          const uint2 eq = v ? in[i] : make_uint2(0, 0);
+          interact_w(c, v, eq.x, eq.y);
+        }
+      } else {
+        for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
+          const uint2 eq = in[i];
+          interact(c, eq.x, eq.y);
+        }
       }
     }
     INET_TMARK(c, 5);
@@ -716,6 +1042,8 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       nh.hi_a = h.hi_a + wa;
       nh.lo_v = h.lo_v + min(k.vtake, h.hi_v - h.lo_v);
       nh.hi_v = h.hi_v + wv;
+      const bool round_failed = (k.qcount & kErrBit) != 0;
+      k.qcount &= ~kErrBit;
       nh.n = k.qcount;
       nh.stop = 0;
       const int32_t parked = ctl->parked_total + k.parked;
@@ -732,7 +1060,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
                                     static_cast<uint32_t>(now - ctl->t_prev));
       ctl->t_prev = now;
       ctl->rounds = r + 1;
-      if (k.err) {
+      if (round_failed) {
         nh.stop = 1;
       } else if (k.qcount == 0) {
         // the trailing no-op loop the reference records (engine.py:222-223)
@@ -784,6 +1112,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     g->communications = ctl->tot_c;
     g->n_residual = base;
     g->parked_total = static_cast<uint32_t>(ctl->parked_total);
+    g->pad[0] = clock_mhz(clk0, gt0);
     if ((ahw > d.cap_agents || hw > d.cap_vars) && g->err == 0) g->err = INET_ERR_ARENA;
   }
   __syncthreads();
@@ -806,6 +1135,373 @@ __device__ __forceinline__ void reduce_body(const NetDesc* __restrict__ nets, ui
     __syncthreads();
     run_net<kTier>(sd, sh, pair, rules, smem);
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Tier C: one net reduced by a thread-block cluster of G CTAs (one per SM),
+// all of its state in the cluster's distributed shared memory.
+//
+// The round structure is the one of run_net, spread over G SMs:
+//   * agent and variable ids are owned round-robin: id i lives at index
+//     i >> log2 G of CTA i & (G-1). Agent loads/stores and slot exchanges are
+//     ld/st/atom.shared::cluster (~0.2 us remote, local ones stay on the SM);
+//     nothing on the round path touches global memory;
+//   * every CTA allocates only ids it owns (its rings and bump pointer), and a
+//     freed id goes back to its owner's ring (free_owned), so the per-CTA
+//     arenas stay balanced whatever the work split;
+//   * every CTA appends the pairs it creates to its own shared-memory queue;
+//     the next round, CTA k takes the pairs whose global index is k mod G,
+//     reading them from their producer's queue;
+//   * a round closes with __syncthreads, a push of the CTA's counters
+//     {pairs queued, interactions, merges, parked delta} into every CTA's
+//     inbox, and one cluster barrier (release/acquire); after it every warp
+//     scans the inbox locally to split the next round;
+//   * the counters rotate over three sets (round r counts into set r%3, its
+//     readers use it between barriers r and r+1, it is cleared in round r+2).
+// Thread 0 of CTA 0 keeps the running totals and writes the per-round row.
+// At the fixpoint the CTAs write their shares back to the global arrays,
+// where the residual equations are compacted in variable-id order.
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_index() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+#ifdef INET_CTIMING
+// Development build: critical-path split of a tier C round, per CTA (thread
+// 0's clock for the barrier, CTA maxima for work and arrival), summed over
+// rounds into the rule-histogram area (tools/cluster_timing.py).
+#define CT_MARK(k)                                                            \
+  do {                                                                        \
+    const long long _t = clock64();                                           \
+    if ((k) == 0) ct_t0 = _t;                                                 \
+    if ((k) == 1) atomicMax(&ct_max[0], static_cast<unsigned long long>(_t - ct_t0)); \
+    if ((k) == 2) atomicMax(&ct_max[1], static_cast<unsigned long long>(_t - ct_t0)); \
+    if ((k) == 3 && threadIdx.x == 0) {                                       \
+      ct_sum[0] += ct_max[0];                                                 \
+      ct_sum[1] += ct_max[1] - ct_max[0];                                     \
+      ct_sum[2] += _t - ct_t0 - ct_max[1];                                    \
+      ct_max[0] = ct_max[1] = 0;                                              \
+    }                                                                         \
+    if ((k) == 0 && threadIdx.x == 0 && ct_t3) ct_sum[3] += _t - ct_t3;       \
+    if ((k) == 3) ct_t3 = _t;                                                 \
+  } while (0)
+#else
+#define CT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
+template <int kBlock>
+__device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_t* pair, const uint32_t* rules,
+                                uint32_t* smem) {
+  constexpr int kTier = kTierC;
+  const SmemPlan plan = plan_smem(sh, kTier);
+  Ctl* ctl = reinterpret_cast<Ctl*>(smem + plan.ctl_off);
+  RoundCtr* ctr3 = reinterpret_cast<RoundCtr*>(smem + plan.agents_off);
+  uint4* inbox = reinterpret_cast<uint4*>(ctr3 + 3);  // [3][16]: {qcount, ints, comms, parked} per CTA
+  uint4* const lagents = reinterpret_cast<uint4*>(smem + plan.cagent_off);
+  uint32_t* const lslots = smem + plan.slots_off;
+  uint2* const lqueue = reinterpret_cast<uint2*>(smem + plan.queue_off);  // [2][res_queue]
+  const uint32_t G = cluster_size(), rank = cluster_rank();
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  Round<kTier> c;
+  c.d = &d;
+  c.ctl = ctl;
+  c.aring = smem + plan.aring_off;
+  c.vring = smem + plan.vring_off;
+  c.amask = sh.ring_a - 1;
+  c.vmask = sh.ring_v - 1;
+  c.pair = pair;
+  c.rules = rules;
+  c.n_labels = sh.n_labels;
+  c.agents = lagents;
+  c.vslot = lslots;
+  // Ids are owned round-robin: CTA k owns k, k+G, k+2G, ... (inputs included)
+  // and keeps id k+G*s at index s of its shared-memory arrays.
+  c.stride = G;
+  c.gshift = __ffs(G) - 1;
+  c.rank = rank;
+  c.a_base = rank;
+  c.v_base = rank;
+  auto owned_below = [&](uint32_t n) -> uint32_t { return n > rank ? (n - rank + G - 1) / G : 0u; };
+  c.cap_agents = min(sh.res_agents, sh.ring_a);
+  c.cap_vars = min(sh.res_vars, sh.ring_v);
+  const uint32_t s0_a = owned_below(d.n_in_agents), s0_v = owned_below(d.n_in_vars);
+  const uint32_t cap_q = sh.res_queue;
+  c.cap_queue = cap_q;
+  const long long clk0 = clock64();
+  const unsigned long long gt0 = globaltimer();
+  // ---- init: this CTA's share of the input agents, empty slots, zero counters
+  const bool fits = s0_a <= c.cap_agents && s0_v <= c.cap_vars && uint64_t(G) * c.cap_agents <= d.cap_agents &&
+                    uint64_t(G) * c.cap_vars <= d.cap_vars;
+  for (uint32_t i = threadIdx.x; i < c.cap_vars; i += kBlock) lslots[i] = kNone;
+  if (fits)
+    for (uint32_t i = threadIdx.x; i < s0_a; i += kBlock) lagents[i] = d.in_agents[rank + G * i];
+  {
+    uint32_t* w = reinterpret_cast<uint32_t*>(ctl);
+    for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += kBlock) w[i] = 0;
+    w = reinterpret_cast<uint32_t*>(ctr3);
+    for (uint32_t i = threadIdx.x; i < 3 * sizeof(RoundCtr) / 4 + 3 * 16 * 4; i += kBlock) w[i] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->agent_bump = s0_a;
+    ctl->var_bump = s0_v;
+  }
+#ifdef INET_CTIMING
+  __shared__ unsigned long long ct_max[2];
+  unsigned long long ct_sum[4] = {0, 0, 0, 0};
+  long long ct_t0 = clock64(), ct_t3 = 0;
+  if (threadIdx.x == 0) ct_max[0] = ct_max[1] = 0;
+#endif
+  cluster_barrier();
+  c.failed = false;
+  uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0;
+  // running totals: thread 0 of CTA 0
+  unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
+  int32_t parked_tot = 0;
+  uint32_t N = d.n_in_eqs, excl = 0, rounds = 1, stop_err = 0;
+  bool stop = false;
+  const bool writer = rank == 0 && threadIdx.x == 0;
+  if (!fits) {
+    stop = true;
+    stop_err = INET_ERR_ARENA;
+  } else if (N == 0) {  // one no-op loop (engine.py:222-223)
+    stop = true;
+    if (writer && d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
+  } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207)
+    stop = true;
+    stop_err = INET_ERR_LOOP_CAP;
+  }
+  for (uint32_t r = 1; !stop; ++r) {
+    RoundCtr* cur = &ctr3[r % 3];
+    c.cur = cur;
+    c.lo_a = lo_a;
+    c.hi_a = hi_a;
+    c.lo_v = lo_v;
+    c.hi_v = hi_v;
+    c.ints = c.comms = 0;
+    c.parked = 0;
+    c.out = lqueue + (r & 1u) * cap_q;
+    if (threadIdx.x == 0) {
+      uint32_t* w = reinterpret_cast<uint32_t*>(&ctr3[(r + 1) % 3]);
+#pragma unroll
+      for (int i = 0; i < static_cast<int>(sizeof(RoundCtr) / 4); ++i) w[i] = 0;
+    }
+    // CTA k takes the pairs whose global index is k mod G: an even sample of
+    // every CTA's queue.
+    if (r == 1) {
+      // the input equations, in any class (communication_phase's first pass)
+      for (uint32_t mb = threadIdx.x & ~31u; rank + G * mb < N; mb += kBlock) {
+        const uint32_t i = rank + G * (mb + lane);
+        const bool v = i < N && !c.failed;
+        const uint2 eq = v ? d.in_eqs[i] : make_uint2(0, 0);
+        const bool act = v && ((eq.x | eq.y) & kVar) == 0;
+        interact_w(c, act, eq.x, eq.y);
+        if (v && !act && !c.failed) link(c, eq.x, eq.y);
+      }
+    } else {
+      const uint2* in = lqueue + ((r - 1) & 1u) * cap_q;
+      for (uint32_t mb = threadIdx.x & ~31u; rank + G * mb < N; mb += kBlock) {
+        const uint32_t i = rank + G * (mb + lane);
+        // segment j of global index i: the last j with excl_j <= i
+        uint32_t j = 0;
+#pragma unroll
+        for (uint32_t step = 8; step; step >>= 1) {
+          const uint32_t cand = j + step;
+          const uint32_t e = __shfl_sync(0xFFFFFFFFu, excl, cand & 31u);
+          if (cand < G && e <= i) j = cand;
+        }
+        const uint32_t ej = __shfl_sync(0xFFFFFFFFu, excl, j);
+        const bool v = i < N && !c.failed;
+        INET_TR(c, 0);
+        const uint2 e = v ? dsmem_ld2(in + (i - ej), j) : make_uint2(0, 0);
+        interact_w(c, v, e.x, e.y);
+        if (v) {
+#ifdef INET_TRACE
+          {
+            const long long t6 = clock64();
+            if (atomicAdd(&inet_trace_count, 1u) < 400u)
+              printf("TR r=%u k=%u t=%u q+ag=%lld pair=%lld alloc=%lld wr+free=%lld exch=%lld settle=%lld\n", r, rank,
+                     threadIdx.x, c.tr[2] - c.tr[0], c.tr[2] - c.tr[1], c.tr[3] - c.tr[2], c.tr[4] - c.tr[3],
+                     c.tr[5] - c.tr[4], t6 - c.tr[5]);
+          }
+#endif
+        }
+      }
+    }
+    CT_MARK(1);
+    {
+      const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
+      const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
+      const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
+      if (lane == 0) {
+        if (wi) atomicAdd(&cur->ints, wi);
+        if (wc) atomicAdd(&cur->comms, wc);
+        if (wp) atomicAdd(&cur->parked, wp);
+      }
+    }
+    // every CTA pushes its round counters into every CTA's inbox
+    __syncthreads();
+    if (threadIdx.x < G)
+      dsmem_st4(&inbox[(r % 3) * 16 + rank], threadIdx.x,
+                make_uint4(cur->qcount, cur->ints, cur->comms, static_cast<uint32_t>(cur->parked)));
+    CT_MARK(2);
+    cluster_barrier();
+    CT_MARK(3);
+    // ---- round r is closed on every CTA: its counters are in the local inbox
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (lane < G) w = inbox[(r % 3) * 16 + lane];
+    const bool err_any = __any_sync(0xFFFFFFFFu, (w.x & kErrBit) != 0);
+    w.x &= ~kErrBit;
+    uint32_t total;
+    excl = warp_excl_scan(w.x, lane, total);
+    {
+      // ids freed to this CTA in round r become allocatable (nothing is dropped)
+      const uint32_t atake = cur->atake, afree = cur->afree, vtake = cur->vtake, vfree = cur->vfree;
+      lo_a += min(atake, hi_a - lo_a);
+      hi_a += afree;
+      lo_v += min(vtake, hi_v - lo_v);
+      hi_v += vfree;
+    }
+    if (rank == 0 && warp == 0) {
+      const uint32_t ri = __reduce_add_sync(0xFFFFFFFFu, w.y);
+      const uint32_t rc = __reduce_add_sync(0xFFFFFFFFu, w.z);
+      const int32_t rp = __reduce_add_sync(0xFFFFFFFFu, static_cast<int32_t>(w.w));
+      if (lane == 0) {
+        tot_i += ri;
+        tot_c += rc;
+        parked_tot += rp;
+        if (d.stats) {
+#ifdef INET_NO_TIMER
+          const unsigned long long now = 0;
+#else
+          const unsigned long long now = globaltimer();
+#endif
+          if (r - 1 < d.cap_rounds)
+            d.stats[r - 1] = make_uint4(ri, rc, total + static_cast<uint32_t>(parked_tot),
+                                        static_cast<uint32_t>(now - t_prev));
+          t_prev = now;
+          if (!err_any && total == 0 && r < d.cap_rounds)
+            d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
+        }
+      }
+    }
+    CT_MARK(0);
+    rounds = r + 1;
+    N = total;
+    if (err_any) {
+      stop = true;
+    } else if (total == 0) {
+      stop = true;  // the trailing no-op loop the reference records (engine.py:222-223)
+    } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
+      stop = true;
+      stop_err = INET_ERR_LOOP_CAP;
+    }
+  }
+#ifdef INET_CTIMING
+  if (threadIdx.x == 0 && d.rule_hist)
+    for (int i = 0; i < 4; ++i)
+      atomicAdd(reinterpret_cast<unsigned long long*>(d.rule_hist) + 32 + i, ct_sum[i]);
+#endif
+  // ---- results. High-water marks of the interleaved id spaces.
+  uint32_t a_hw = d.n_in_agents, v_hw = d.n_in_vars;
+  uint32_t e_code = 0, e_a = 0, e_b = 0;
+  if (lane < G) {
+    const uint32_t ab = dsmem_ld(&ctl->agent_bump, lane), vb = dsmem_ld(&ctl->var_bump, lane);
+    if (ab) a_hw = max(a_hw, lane + G * (min(ab, c.cap_agents) - 1) + 1);
+    if (vb) v_hw = max(v_hw, lane + G * (min(vb, c.cap_vars) - 1) + 1);
+    e_code = dsmem_ld(&ctl->err_code, lane);
+    e_a = dsmem_ld(&ctl->err_a, lane);
+    e_b = dsmem_ld(&ctl->err_b, lane);
+  }
+  a_hw = min(__reduce_max_sync(0xFFFFFFFFu, a_hw), d.cap_agents);
+  v_hw = min(__reduce_max_sync(0xFFFFFFFFu, v_hw), d.cap_vars);
+  const uint32_t e_mask = __ballot_sync(0xFFFFFFFFu, e_code != 0);
+  const uint32_t e_src = e_mask ? __ffs(e_mask) - 1 : 0;
+  e_code = __shfl_sync(0xFFFFFFFFu, e_code, e_src);
+  e_a = __shfl_sync(0xFFFFFFFFu, e_a, e_src);
+  e_b = __shfl_sync(0xFFFFFFFFu, e_b, e_src);
+  // write this CTA's share of the agents and slots back to the global arrays
+  {
+    const uint32_t na = min(ctl->agent_bump, c.cap_agents), nv = min(ctl->var_bump, c.cap_vars);
+    for (uint32_t i = threadIdx.x; i < na; i += kBlock) d.agents[rank + G * i] = lagents[i];
+    for (uint32_t i = threadIdx.x; i < nv; i += kBlock) d.vslot[rank + G * i] = lslots[i];
+    // ids below the high-water mark that this CTA never handed out read as free
+    const uint32_t nv_hw = owned_below(v_hw);
+    for (uint32_t i = nv + threadIdx.x; i < nv_hw; i += kBlock) d.vslot[rank + G * i] = kNone;
+  }
+  cluster_barrier();
+  // residual parked equations in variable-id order: CTA k compacts slice k
+  const uint32_t s_lo = static_cast<uint32_t>(uint64_t(v_hw) * rank / G);
+  const uint32_t s_hi = static_cast<uint32_t>(uint64_t(v_hw) * (rank + 1) / G);
+  uint32_t mine = 0;
+  for (uint32_t x = s_lo + threadIdx.x; x < s_hi; x += kBlock) mine += d.vslot[x] != kNone;
+  mine = __reduce_add_sync(0xFFFFFFFFu, mine);
+  if (threadIdx.x == 0) ctl->scratch[33] = 0;
+  __syncthreads();
+  if (lane == 0 && mine) atomicAdd(&ctl->scratch[33], mine);
+  cluster_barrier();
+  uint32_t n_res;
+  {
+    const uint32_t cnt = lane < G ? dsmem_ld(&ctl->scratch[33], lane) : 0;
+    const uint32_t ex = warp_excl_scan(cnt, lane, n_res);
+    uint32_t base = __shfl_sync(0xFFFFFFFFu, ex, rank);
+    for (uint32_t c0 = s_lo; c0 < s_hi; c0 += kBlock) {
+      const uint32_t x = c0 + threadIdx.x;
+      const uint32_t v = x < s_hi ? d.vslot[x] : kNone;
+      uint32_t off;
+      const uint32_t tot = block_scan_flag(v != kNone, ctl->scratch, &off);
+      if (v != kNone && base + off < d.cap_vars) d.residual[base + off] = make_uint2(kVar | x, v);
+      base += tot;
+    }
+  }
+  if (writer) {
+    NetCtl* g = d.ctl;
+    g->agent_bump = a_hw;
+    g->var_bump = v_hw;
+    g->err = stop_err ? stop_err : e_code;
+    g->err_a = stop_err ? 0 : e_a;
+    g->err_b = stop_err ? 0 : e_b;
+    g->rounds = rounds;
+    g->interactions = tot_i;
+    g->communications = tot_c;
+    g->n_residual = n_res;
+    g->parked_total = static_cast<uint32_t>(parked_tot);
+    g->pad[0] = clock_mhz(clk0, gt0);
+  }
+  cluster_barrier();  // no CTA leaves while another may still read its shared memory
+}
+
+// Kernel body of tier C: cluster i reduces net i.
+template <int kBlock>
+__device__ __forceinline__ void reduce_cluster_body(const NetDesc* __restrict__ nets, uint32_t n_nets,
+                                                    const uint32_t* __restrict__ blob, const Shape& sh,
+                                                    uint32_t* smem, NetDesc& sd) {
+  for (uint32_t i = threadIdx.x; i < sh.rule_words; i += kBlock) smem[i] = blob[4 + i];
+  const uint32_t pair_words = (sh.n_labels * sh.n_labels + 1) / 2;
+  const uint16_t* pair = reinterpret_cast<const uint16_t*>(smem);
+  const uint32_t* rules = smem + pair_words;
+  const uint32_t net = cluster_index();
+  if (threadIdx.x == 0 && net < n_nets) sd = nets[net];
+  __syncthreads();
+  if (net < n_nets) run_net_cluster<kBlock>(sd, sh, pair, rules, smem);
 }
 
 }  // namespace inetdev

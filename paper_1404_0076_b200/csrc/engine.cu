@@ -29,6 +29,7 @@ namespace {
 
 using inetdev::Shape;
 
+using inetdev::kTierC;
 using inetdev::kTierG;
 using inetdev::kTierM;
 using inetdev::kTierS;
@@ -42,7 +43,30 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const NetDesc* __restric
   inetdev::reduce_body<kBlock, kTier>(nets, n_nets, blob, sh, smem, sd);
 }
 
+template <int kBlock>
+__global__ void __launch_bounds__(kBlock) reduce_cluster_kernel(const NetDesc* __restrict__ nets, uint32_t n_nets,
+                                                                const uint32_t* __restrict__ blob, Shape sh) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ NetDesc sd;
+  inetdev::reduce_cluster_body<kBlock>(nets, n_nets, blob, sh, smem, sd);
+}
+
 using KernelFn = void (*)(const NetDesc*, uint32_t, const uint32_t*, Shape);
+
+KernelFn pick_cluster_kernel(uint32_t threads) {
+  switch (threads) {
+    case 64:
+      return reduce_cluster_kernel<64>;
+    case 128:
+      return reduce_cluster_kernel<128>;
+    case 256:
+      return reduce_cluster_kernel<256>;
+    case 512:
+      return reduce_cluster_kernel<512>;
+    default:
+      return reduce_cluster_kernel<1024>;
+  }
+}
 
 template <int kTier>
 KernelFn pick_kernel_t(uint32_t threads) {
@@ -61,6 +85,7 @@ KernelFn pick_kernel_t(uint32_t threads) {
 }
 
 KernelFn pick_kernel(uint32_t threads, int tier) {
+  if (tier == kTierC) return pick_cluster_kernel(threads);
   if (tier == kTierS) return pick_kernel_t<kTierS>(threads);
   if (tier == kTierM) return pick_kernel_t<kTierM>(threads);
   return pick_kernel_t<kTierG>(threads);
@@ -112,6 +137,7 @@ struct inet_ctx {
   uint64_t io_h2d = 0, io_d2h = 0;
   uint32_t cap_agents = 0, cap_vars = 0, cap_queue = 0, cap_rounds = 0;
   int tier = kTierG;  // tier of the last successful run
+  uint32_t cluster_g = 1;  // CTAs per net of the last run (tier C)
   Shape shape{};
   bool collect_stats = false;
   bool reduced = false;
@@ -128,7 +154,8 @@ struct inet_ctx {
   int jit_mode = 1;  // 0 = prebuilt interpreter only
   bool last_jit = false;
   std::string jit_log;
-  std::map<std::pair<int, uint32_t>, std::pair<cudaLibrary_t, cudaKernel_t>> jit_kernels;
+  std::map<std::tuple<int, uint32_t, int>, std::pair<cudaLibrary_t, cudaKernel_t>> jit_kernels;
+  int jit_style = -1;  // -1: per tier (measured defaults); env INET_B200_JITSTYLE overrides
 };
 
 inline uint32_t hist_stride(const inet_ctx* c) { return std::max(c->n_rules, 128u); }
@@ -179,6 +206,7 @@ int inet_ctx_create(int device, inet_ctx** out) {
   auto* c = new inet_ctx();
   c->device = device;
   if (const char* e = std::getenv("INET_B200_JIT")) c->jit_mode = std::atoi(e);
+  if (const char* e = std::getenv("INET_B200_JITSTYLE")) c->jit_style = std::atoi(e);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
     delete c;
@@ -332,16 +360,29 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
   return c->n_nets >= 16 ? 512 : 1024;
 }
 
+// CTA size of tier C (one CTA per SM of the cluster).
+uint32_t cluster_threads(const inet_cfg* cfg) {
+  const uint32_t t = cfg && cfg->threads ? cfg->threads : 512;
+  if (t <= 64) return 64;
+  if (t <= 128) return 128;
+  if (t <= 256) return 256;
+  if (t <= 512) return 512;
+  return 1024;
+}
+
 // One attempt at the current capacities and tier: one kernel launch, timed.
 // Rule-set specialised kernel for (tier, threads), compiled on first use;
 // nullptr when NVRTC is unavailable or compilation failed (then the prebuilt
 // interpreter runs).
 const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
   if (!c->jit_mode) return nullptr;
-  const auto key = std::make_pair(tier, threads);
+  // code style per tier: straight-line cases where the rewrite is issue-bound
+  // (S, M, G); a uniform memory phase where remote latency dominates (C)
+  const int style = c->jit_style >= 0 ? c->jit_style : (tier == kTierC ? 1 : 0);
+  const auto key = std::make_tuple(tier, threads, style);
   auto it = c->jit_kernels.find(key);
   if (it != c->jit_kernels.end()) return reinterpret_cast<const void*>(it->second.second);
-  const std::string src = inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads);
+  const std::string src = inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style);
   std::vector<char> cubin;
   if (inetjit::compile_cubin(src, cubin, c->jit_log) != 0) {
     std::fprintf(stderr, "inet_b200: rule-set JIT unavailable, using the prebuilt kernels: %s\n", c->jit_log.c_str());
@@ -362,7 +403,7 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
 }
 
 int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
-  const uint32_t threads = auto_threads(c, cfg);
+  const uint32_t threads = tier == kTierC ? cluster_threads(cfg) : auto_threads(c, cfg);
   sh.threads = threads;
   const void* jk = jit_kernel(c, tier, threads);
   const void* fn = jk ? jk : reinterpret_cast<const void*>(pick_kernel(threads, tier));
@@ -373,16 +414,41 @@ int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
   if (smem + sizeof(NetDesc) > size_t(max_optin)) return INET_ERR_UNSUPPORTED;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), smem);
-  uint32_t grid = std::max(1, dev_sms * std::max(per_sm, 1));
-  grid = std::min(grid, c->n_nets);
-  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   const NetDesc* a_nets = static_cast<const NetDesc*>(c->d_desc.p);
   uint32_t a_n = c->n_nets;
   const uint32_t* a_blob = static_cast<const uint32_t*>(c->d_blob.p);
   void* args[] = {&a_nets, &a_n, &a_blob, &sh};
-  CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, c->stream));
+  if (tier == kTierC) {
+    // one cluster of G CTAs per net (G > 8 needs the non-portable opt-in)
+    const uint32_t G = c->cluster_g;
+    if (G > 8) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(G * c->n_nets);
+    lc.blockDim = dim3(threads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int n_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&n_clusters, fn, &lc) != cudaSuccess || n_clusters < 1) {
+      cudaGetLastError();
+      return INET_ERR_UNSUPPORTED;
+    }
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(cudaLaunchKernelExC(&lc, fn, args));
+  } else {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), smem);
+    uint32_t grid = std::max(1, dev_sms * std::max(per_sm, 1));
+    grid = std::min(grid, c->n_nets);
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, c->stream));
+  }
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
   CUDA_TRY(cudaEventSynchronize(c->ev1));
   CUDA_TRY(cudaEventElapsedTime(ms, c->ev0, c->ev1));
@@ -453,6 +519,24 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
       if (st != INET_OK && st != INET_ERR_UNSUPPORTED) return st;
     }
   }
+  // Large single nets: a cluster of G CTAs sharing their shared memory (tier C).
+  // Its arenas are fixed by shared memory; a net that outgrows them falls
+  // through to the single-CTA tiers.
+  const uint32_t want_g = cfg ? cfg->ctas_per_net : 0;
+  if (!done && want_g >= 2 && c->n_nets <= 64) {
+    uint32_t G = 2;  // a power of two (ids are owned round-robin: owner = id & (G - 1))
+    while (G * 2 <= std::min<uint32_t>(want_g, 16)) G *= 2;
+    Shape sh = base_shape(c, max_loops);
+    sh.res_agents = 4096;
+    sh.res_vars = 4096;
+    sh.res_queue = 4096;
+    sh.ring_a = 4096;
+    sh.ring_v = 4096;
+    c->cluster_g = G;
+    int st = attempt_tier(kTierC, sh, G * sh.res_agents, G * sh.res_vars, 1);
+    if (st == INET_OK && !any_oom()) done = true;
+    else if (st != INET_OK && st != INET_ERR_UNSUPPORTED) return st;
+  }
   if (!done && !user_caps && c->n_nets <= 148 && c->max_in_agents < 32768 && c->max_in_vars < 16384) {
     Shape sh = base_shape(c, max_loops);
     sh.res_vars = 14336;
@@ -499,6 +583,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     s.cap_vars = c->cap_vars;
     s.tier = static_cast<uint32_t>(c->tier);
     s.jit = c->last_jit ? 1u : 0u;
+    s.sm_mhz = k.pad[0];
     if (first == INET_OK && k.err) first = static_cast<int>(k.err);
   }
   c->reduced = true;
@@ -589,7 +674,9 @@ int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t th
   if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
   std::vector<char> cubin;
   std::string msg;
-  const int rc = inetjit::compile_cubin(inetjit::kernel_source(blob, n_words, tier, threads), cubin, msg);
+  int style = tier == kTierC ? 1 : 0;
+  if (const char* e = std::getenv("INET_B200_JITSTYLE")) style = std::atoi(e);
+  const int rc = inetjit::compile_cubin(inetjit::kernel_source(blob, n_words, tier, threads, style), cubin, msg);
   if (log && log_len) {
     std::strncpy(log, msg.c_str(), log_len - 1);
     log[log_len - 1] = 0;

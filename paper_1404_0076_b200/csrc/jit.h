@@ -8,9 +8,10 @@
 namespace inetjit {
 
 // CUDA source of the per-rule rewrites (jit_apply) for a rule blob.
-std::string generate_rules(const uint32_t* blob, size_t n_words);
+std::string generate_rules(const uint32_t* blob, size_t n_words, int style = 0);
 // Complete translation unit: device code + rewrites + one kernel `inet_jit_kernel`.
-std::string kernel_source(const uint32_t* blob, size_t n_words, int tier, uint32_t block);
+// style: 0 straight-line cases, 1 per-lane uniform memory phase, 2 warp-collective
+std::string kernel_source(const uint32_t* blob, size_t n_words, int tier, uint32_t block, int style = 0);
 // NVRTC loadable?
 bool available();
 // Compile (or fetch from the on-disk cache) to an sm_100a cubin; 0 on success.

@@ -57,6 +57,7 @@ class EngineConfig:
     validate_phases: bool = False
     device: int = 0
     threads: int = 0
+    ctas_per_net: int = 0
 
 
 @dataclass(slots=True)
@@ -198,6 +199,7 @@ def native_cfg(cfg: EngineConfig) -> _native.Cfg:
     k.max_loops = max(0, min(int(cfg.max_loops), 0xFFFFFFFE))
     k.collect_stats = 1 if cfg.collect_stats else 0
     k.threads = cfg.threads
+    k.ctas_per_net = cfg.ctas_per_net
     return k
 
 

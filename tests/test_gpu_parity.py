@@ -214,3 +214,51 @@ def test_collect_stats_off_and_arena_growth():
         ctx._blob_key = None
     assert code == _native.OK
     assert st.interactions == 50_515 and st.cap_agents > 128
+
+
+# ---- tier C: one net on a thread-block cluster (distributed shared memory) ----
+
+@pytest.mark.parametrize("g", [2, 4, 16])
+def test_cluster_tier_fixtures(g):
+    """Every reference fixture through the cluster engine: same normal form and interaction count."""
+    for case in CASES:
+        config, rules = _case_inputs(case)
+        kw = dict(case.get("engine_config", {}))
+        kw["ctas_per_net"] = g
+        cfg = EngineConfig(**kw)
+        if "error" in case:
+            with pytest.raises(getattr(errors, case["error"])) as ei:
+                evaluate(config, rules, cfg)
+            if case.get("error_pair"):
+                assert list(ei.value.pair) == case["error_pair"], case["name"]
+            continue
+        res = evaluate(config, rules, cfg)
+        assert res.total_interactions == case["interactions"], case["name"]
+        assert _sha(print_configuration(res.final)) == case["print_sha256"], case["name"]
+        _check_loops(res)
+
+
+@pytest.mark.parametrize("params,interactions,communications,loops,sha", [
+    ((3, 8), 5_574_030, 4_177_966, 14_235, "b85606c71178de4b"),
+    ((3, 10), 89_404_824, 67_043_382, 57_227, "981fd9bfe283f466"),
+])
+def test_cluster_tier_large_ackermann(params, interactions, communications, loops, sha):
+    prog = programs.program("ackermann")
+    res = evaluate(prog.build_input(*params), prog.rules, EngineConfig(ctas_per_net=16))
+    assert res.total_interactions == interactions
+    assert res.total_communications == communications
+    assert len(res.loops) == loops
+    assert _sha(print_configuration(res.final)).startswith(sha)
+    _check_loops(res)
+
+
+def test_cluster_tier_random_arith_against_oracle():
+    rules = programs.load_rules("arith")
+    orules = O.rules_for("arith")
+    rng = random.Random(99)
+    for _ in range(40):
+        net = _random_arith_net(rng, rules.symbols, rng.choice([8, 40, 200, 1000]))
+        res = evaluate(net, rules, EngineConfig(ctas_per_net=8, collect_stats=False))
+        want = O.run_config(net, orules, collect=False)
+        assert res.total_interactions == want.interactions
+        assert print_configuration(res.final) == want.printed()

@@ -13,6 +13,7 @@ ap.add_argument("--nets", type=int, default=4096)
 ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--jit", type=int, default=1)
+ap.add_argument("--g", type=int, default=0, help="CTAs per net (tier C cluster)")
 a = ap.parse_args()
 spec = {"a38": ("ackermann", (3, 8), 1), "a310": ("ackermann", (3, 10), 1), "fib18": ("fibonacci", (18,), 1),
         "batch": ("ackermann", (3, 6), a.nets)}[a.workload]
@@ -22,8 +23,8 @@ ctx = _native.Context(0)
 ctx.set_jit(bool(a.jit))
 ctx.load_rules(prep.blob)
 ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
-k = engine.native_cfg(EngineConfig(collect_stats=False, threads=a.threads))
+k = engine.native_cfg(EngineConfig(collect_stats=False, threads=a.threads, ctas_per_net=a.g))
 for _ in range(a.repeat):
     code, ms = ctx.reduce(k)
     st = ctx.stats(0)
-    print(a.workload, "code", code, "ms", ms, ctx.totals(), "tier", st.tier, "jit", st.jit, "hw", st.agent_hw, st.var_hw)
+    print(a.workload, "code", code, "ms", ms, ctx.totals(), "tier", st.tier, "jit", st.jit, "hw", st.agent_hw, st.var_hw, "MHz", st.sm_mhz)
