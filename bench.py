@@ -384,7 +384,8 @@ def run_ours(args) -> None:
                 flush_l2()
                 best.append(c2.rerun(kk))
             ms = min(best)
-            singles[label] = {"interactions": golden, "rounds": st.rounds, "device_ms": ms, "tier": "SMG"[st.tier],
+            singles[label] = {"interactions": golden, "rounds": st.rounds, "device_ms": ms, "tier": "SMGC"[st.tier],
+                              "sm_mhz": st.sm_mhz,
                               "agent_hw": st.agent_hw, "var_hw": st.var_hw,
                               "interactions_per_s": golden / (ms / 1000.0),
                               "us_per_round": 1000.0 * ms / max(st.rounds, 1)}

@@ -57,6 +57,7 @@ constexpr int kEnvNone = 22;
 constexpr int kEnvSize = 23;  // sources 0..22 (22 = none)
 constexpr int kRuleWords = 16;
 constexpr int kFastEq = 4;  // rhs equations linked with overlapped exchanges
+constexpr uint32_t kMbox = 64;  // tier C: ids one CTA can mail to one owner per round (then direct frees)
 
 enum : int { kTierS = 0, kTierM = 1, kTierG = 2, kTierC = 3 };
 
@@ -237,6 +238,11 @@ struct Round {
   uint32_t lo_a, hi_a, lo_v, hi_v;  // ring windows available this round
   uint32_t a_base, v_base, stride;  // tier C: bump sequence s -> id base + stride * s
   uint32_t rank, gshift;            // tier C: this CTA's rank in the cluster, log2 G
+  uint32_t* outc;                   // tier C: ids mailed this round per owner: agents [0,16), vars [16,32)
+  uint32_t* mbox_a;                 // tier C: mailboxes of this round, [src][kMbox] (owner's layout)
+  uint32_t* mbox_v;
+  uint2* inq;                       // tier C: next round's input queues, [producer][qj] (consumer's layout)
+  uint32_t qj;
   uint32_t ints, comms;
   int32_t parked;
   bool failed;
@@ -251,6 +257,9 @@ struct Round {
 
 #ifdef INET_TRACE
 __device__ unsigned int inet_trace_count;
+#ifndef INET_TRACE_R0
+#define INET_TRACE_R0 2
+#endif
 #define INET_TR(c, k) ((c).tr[k] = clock64())
 #else
 #define INET_TR(c, k) \
@@ -323,19 +332,29 @@ __device__ __forceinline__ uint32_t dsmem_ld(const void* p, uint32_t rank) {
 // A CTA never owns more ids than its ring holds, so nothing is dropped.
 template <int kTier>
 __device__ __forceinline__ void free_owned(Round<kTier>& c, uint32_t id, uint32_t* fpos, uint32_t* ring, uint32_t mask,
-                                           uint32_t* cnt) {
+                                           uint32_t* cnt, uint32_t* outc, uint32_t* mbox) {
   const uint32_t k = id & (c.stride - 1);
   if (k == c.rank) {
     const uint32_t pos = atomicAdd(fpos, 1u);
     ring[pos & mask] = id;
     atomicAdd(cnt, 1u);
-  } else {
-    const uint32_t pos = dsmem_atom_add(fpos, k, 1u);
-    dsmem_st(&ring[pos & mask], k, id);
-    dsmem_red_add(cnt, k, 1u);
+    return;
   }
+  // mail it: a local counter and one remote store; the owner moves its mail
+  // into its ring next round (allocatable the round after)
+#ifdef INET_NO_MBOX
+  const uint32_t p = kMbox;
+#else
+  const uint32_t p = atomicAdd(&outc[k], 1u);
+#endif
+  if (p < kMbox) {
+    dsmem_st(&mbox[c.rank * kMbox + p], k, id);
+    return;
+  }
+  const uint32_t pos = dsmem_atom_add(fpos, k, 1u);  // mailbox full: straight into the owner's ring
+  dsmem_st(&ring[pos & mask], k, id);
+  dsmem_red_add(cnt, k, 1u);
 }
-
 
 // ---- agent and variable-slot access -----------------------------------------
 // Tiers S/M/G address one array; tier C spreads both over the cluster's shared
@@ -421,7 +440,7 @@ __device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, Claim&
 template <int kTier>
 __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
   if constexpr (kTier == kTierC) {
-    free_owned(c, a, &c.ctl->fpos_a, reinterpret_cast<uint32_t*>(c.aring), c.amask, &c.cur->afree);
+    free_owned(c, a, &c.ctl->fpos_a, reinterpret_cast<uint32_t*>(c.aring), c.amask, &c.cur->afree, c.outc, c.mbox_a);
     return;
   }
   const uint32_t f = atomicAdd(&c.cur->afree, 1u);
@@ -432,7 +451,8 @@ __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
 template <int kTier>
 __device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
   if constexpr (kTier == kTierC) {
-    free_owned(c, x, &c.ctl->fpos_v, reinterpret_cast<uint32_t*>(c.vring), c.vmask, &c.cur->vfree);
+    free_owned(c, x, &c.ctl->fpos_v, reinterpret_cast<uint32_t*>(c.vring), c.vmask, &c.cur->vfree, c.outc + 16,
+               c.mbox_v);
     return;
   }
   const uint32_t f = atomicAdd(&c.cur->vfree, 1u);
@@ -440,10 +460,25 @@ __device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
   if (pos - c.lo_v <= c.vmask) c.vring[pos & c.vmask] = x;
 }
 
-// Queue an active pair.
+__device__ __forceinline__ void dsmem_st2(const void* p, uint32_t rank, uint2 v) {
+  asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" ::"r"(dsmem_addr(p, rank)), "r"(v.x), "r"(v.y) : "memory");
+}
+
+// Queue an active pair. Tier C deals a CTA's pairs round-robin over the
+// cluster (the p-th to CTA (p + rank) mod G, slot p / G) straight into the
+// consumer's shared memory, so next round every CTA reads its pairs locally.
 template <int kTier>
 __device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_t r) {
   const uint32_t p = atomicAdd(&c.cur->qcount, 1u);
+  if constexpr (kTier == kTierC) {
+    const uint32_t s = (p & ~kErrBit) >> c.gshift;
+    if (s >= c.qj) {
+      fail(c, INET_ERR_ARENA, 2);
+      return;
+    }
+    dsmem_st2(&c.inq[c.rank * c.qj + s], (p + c.rank) & (c.stride - 1), make_uint2(l, r));
+    return;
+  }
   if (p >= c.cap_queue) {
     fail(c, INET_ERR_ARENA, 2);
     return;
@@ -457,6 +492,10 @@ __device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_
 // Warp-collective push: every lane calls it, lanes with `pu` push (l, r).
 template <int kTier>
 __device__ __forceinline__ void warp_push(Round<kTier>& c, bool pu, uint32_t l, uint32_t r) {
+  if constexpr (kTier == kTierC) {
+    if (pu) push_active(c, l, r);
+    return;
+  }
   const uint32_t m = __ballot_sync(0xFFFFFFFFu, pu);
   if (!m) return;
   const uint32_t lane = threadIdx.x & 31u, leader = __ffs(m) - 1;
@@ -637,6 +676,41 @@ __device__ __forceinline__ void jit_warp(Round<kTier>& c, bool valid, uint32_t l
 template <int kTier>
 __device__ __forceinline__ void jit_apply(Round<kTier>& c, uint32_t rule, const uint4& A, const uint4& B, uint32_t l,
                                           uint32_t r);
+
+// Both claims of a rewrite with their ring atomics issued back to back.
+template <uint32_t MF, uint32_t MX, int kTier>
+__device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uint32_t nx, uint32_t (&f)[MF],
+                                               uint32_t (&g)[MX]) {
+  if ((nf | nx) == 0) return true;
+  const uint32_t tv = nf ? atomicAdd(&c.cur->vtake, nf) : 0u;
+  const uint32_t ta = nx ? atomicAdd(&c.cur->atake, nx) : 0u;
+  const uint32_t av_v = c.hi_v - c.lo_v, av_a = c.hi_a - c.lo_a;
+  const uint32_t gv = tv < av_v ? min(av_v - tv, nf) : 0u, ga = ta < av_a ? min(av_a - ta, nx) : 0u;
+  uint32_t bv = 0, ba = 0;
+  if (gv < nf) {
+    bv = atomicAdd(&c.ctl->var_bump, nf - gv);
+    if (bv + (nf - gv) > c.cap_vars) {
+      fail(c, INET_ERR_ARENA, 1);
+      return false;
+    }
+  }
+  if (ga < nx) {
+    ba = atomicAdd(&c.ctl->agent_bump, nx - ga);
+    if (ba + (nx - ga) > c.cap_agents) {
+      fail(c, INET_ERR_ARENA, 0);
+      return false;
+    }
+  }
+#pragma unroll
+  for (uint32_t j = 0; j < MF; ++j)
+    if (j < nf)
+      f[j] = kVar | (j < gv ? static_cast<uint32_t>(c.vring[(c.lo_v + tv + j) & c.vmask]) : bump_var(c, bv + (j - gv)));
+#pragma unroll
+  for (uint32_t j = 0; j < MX; ++j)
+    if (j < nx)
+      g[j] = j < ga ? static_cast<uint32_t>(c.aring[(c.lo_a + ta + j) & c.amask]) : bump_agent(c, ba + (j - ga));
+  return true;
+}
 
 // Active pair -> queue (returns false); otherwise the slot key and the parked value.
 template <int kTier>
@@ -833,6 +907,7 @@ __device__ __forceinline__ uint32_t block_scan_flag(bool flag, uint32_t* warp_to
 //   rule table | Ctl | agent ring | var ring | [S: agents] | [S,M: slots] | [S,M: 2 queues]
 struct SmemPlan {
   uint32_t ctl_off, aring_off, vring_off, agents_off, slots_off, queue_off, env_off, cagent_off, words;
+  uint32_t outc_off, inbox_off, mbox_off;  // tier C
 };
 
 __host__ __device__ inline uint32_t align4(uint32_t w) { return (w + 3u) & ~3u; }
@@ -841,7 +916,8 @@ __host__ __device__ inline uint32_t align4(uint32_t w) { return (w + 3u) & ~3u; 
 //   S: rules | Ctl | u16 rings | agents | slots | 2 packed queues
 //   M: rules | Ctl | u16 rings | slots | 2 packed queues        (agents global)
 //   G: rules | Ctl | u32 rings                                   (rest global)
-//   C: rules | Ctl | u32 rings | 3 counter sets + inbox | slots | 2 queues | agents
+//   C: rules | Ctl | u32 rings | 3 counter sets | 3 mail counts | 3 inboxes |
+//      2x2 mailboxes | slots | 2 input queues [16][res_queue] | agents
 //      (this CTA's share of the cluster-wide arrays)
 __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
   const uint32_t ring_bytes = tier >= kTierG ? 4u : 2u;
@@ -850,14 +926,24 @@ __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
   p.aring_off = p.ctl_off + align4(sizeof(Ctl) / 4);
   p.vring_off = p.aring_off + align4((sh.ring_a * ring_bytes + 3) / 4);
   p.agents_off = p.vring_off + align4((sh.ring_v * ring_bytes + 3) / 4);
-  p.slots_off = p.agents_off + (tier == kTierS ? 4 * sh.res_agents
-                                : tier == kTierC ? align4(3 * sizeof(RoundCtr) / 4 + 3 * 16 * 4) : 0);
+  p.outc_off = p.inbox_off = p.mbox_off = 0;
+  if (tier == kTierC) {
+    p.outc_off = p.agents_off + align4(3 * sizeof(RoundCtr) / 4);
+    p.inbox_off = p.outc_off + 3 * 32;
+    p.mbox_off = p.inbox_off + 3 * 16 * 8;
+    p.slots_off = p.mbox_off + 2 * 2 * 16 * kMbox;
+    p.queue_off = p.slots_off + align4(sh.res_vars);
+    p.env_off = p.queue_off + 2 * 16 * sh.res_queue * 2;
+    p.cagent_off = p.env_off;
+    p.words = p.cagent_off + 4 * sh.res_agents;
+    return p;
+  }
+  p.slots_off = p.agents_off + (tier == kTierS ? 4 * sh.res_agents : 0);
   const bool res_slots = tier != kTierG;
   p.queue_off = p.slots_off + (res_slots ? align4(sh.res_vars) : 0);
-  const uint32_t qwords = tier == kTierC ? 2 * 2 * sh.res_queue : 2 * sh.res_queue;  // C: uint2 entries
-  p.env_off = p.queue_off + (res_slots ? align4(qwords) : 0);
+  p.env_off = p.queue_off + (res_slots ? align4(2 * sh.res_queue) : 0);
   p.cagent_off = p.env_off;
-  p.words = p.cagent_off + (tier == kTierC ? 4 * sh.res_agents : 0);
+  p.words = p.cagent_off;
   return p;
 }
 
@@ -1214,10 +1300,12 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   const SmemPlan plan = plan_smem(sh, kTier);
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + plan.ctl_off);
   RoundCtr* ctr3 = reinterpret_cast<RoundCtr*>(smem + plan.agents_off);
-  uint4* inbox = reinterpret_cast<uint4*>(ctr3 + 3);  // [3][16]: {qcount, ints, comms, parked} per CTA
+  uint32_t* const outc3 = smem + plan.outc_off;                          // [3][32] ids mailed per owner
+  uint4* const inbox = reinterpret_cast<uint4*>(smem + plan.inbox_off);  // [3][16][2] counters per source CTA
+  uint32_t* const mbox = smem + plan.mbox_off;                           // [2 parity][2 kind][16 src][kMbox]
   uint4* const lagents = reinterpret_cast<uint4*>(smem + plan.cagent_off);
   uint32_t* const lslots = smem + plan.slots_off;
-  uint2* const lqueue = reinterpret_cast<uint2*>(smem + plan.queue_off);  // [2][res_queue]
+  uint2* const lqueue = reinterpret_cast<uint2*>(smem + plan.queue_off);  // [2 parity][16 producer][res_queue]
   const uint32_t G = cluster_size(), rank = cluster_rank();
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   Round<kTier> c;
@@ -1243,8 +1331,9 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   c.cap_agents = min(sh.res_agents, sh.ring_a);
   c.cap_vars = min(sh.res_vars, sh.ring_v);
   const uint32_t s0_a = owned_below(d.n_in_agents), s0_v = owned_below(d.n_in_vars);
-  const uint32_t cap_q = sh.res_queue;
+  const uint32_t cap_q = sh.res_queue;  // pairs one producer can deal to one consumer per round
   c.cap_queue = cap_q;
+  c.qj = cap_q;
   const long long clk0 = clock64();
   const unsigned long long gt0 = globaltimer();
   // ---- init: this CTA's share of the input agents, empty slots, zero counters
@@ -1257,7 +1346,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     uint32_t* w = reinterpret_cast<uint32_t*>(ctl);
     for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += kBlock) w[i] = 0;
     w = reinterpret_cast<uint32_t*>(ctr3);
-    for (uint32_t i = threadIdx.x; i < 3 * sizeof(RoundCtr) / 4 + 3 * 16 * 4; i += kBlock) w[i] = 0;
+    for (uint32_t i = threadIdx.x; i < plan.mbox_off - plan.agents_off; i += kBlock) w[i] = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1298,11 +1387,50 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     c.hi_v = hi_v;
     c.ints = c.comms = 0;
     c.parked = 0;
-    c.out = lqueue + (r & 1u) * cap_q;
-    if (threadIdx.x == 0) {
-      uint32_t* w = reinterpret_cast<uint32_t*>(&ctr3[(r + 1) % 3]);
+    c.inq = lqueue + (r & 1u) * 16 * cap_q;
+    c.outc = outc3 + (r % 3) * 32;
+    c.mbox_a = mbox + (r & 1u) * 2 * 16 * kMbox;
+    c.mbox_v = c.mbox_a + 16 * kMbox;
+    if (threadIdx.x < 32) {
+      if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(&ctr3[(r + 1) % 3])[threadIdx.x] = 0;
+      outc3[((r + 1) % 3) * 32 + threadIdx.x] = 0;
+    }
+    // mail of round r-1: move the ids other CTAs freed for this one into its rings
+    // (the top warps do it; pairs go to the low threads first)
+    if (r > 1) {
+      const uint32_t ma = lane < G ? min(inbox[((r - 1) % 3) * 32 + 2 * lane + 1].x, kMbox) : 0u;
+      const uint32_t mv = lane < G ? min(inbox[((r - 1) % 3) * 32 + 2 * lane + 1].y, kMbox) : 0u;
+      uint32_t ta, tv;
+      const uint32_t xa = warp_excl_scan(ma, lane, ta), xv = warp_excl_scan(mv, lane, tv);
+      const uint32_t* pm = mbox + ((r - 1) & 1u) * 2 * 16 * kMbox;
+      const uint32_t nw = kBlock / 32;
+      for (uint32_t eb = (nw - 1 - warp) * 32; eb < ta + tv; eb += kBlock) {
+        const uint32_t e = eb + lane;
+        const bool is_a = e < ta;
+        const uint32_t q = is_a ? e : e - ta;
+        uint32_t j = 0;
 #pragma unroll
-      for (int i = 0; i < static_cast<int>(sizeof(RoundCtr) / 4); ++i) w[i] = 0;
+        for (uint32_t step = 8; step; step >>= 1) {
+          const uint32_t cand = j + step;
+          const uint32_t ea = __shfl_sync(0xFFFFFFFFu, xa, cand & 31u);
+          const uint32_t ev = __shfl_sync(0xFFFFFFFFu, xv, cand & 31u);
+          if (cand < G && (is_a ? ea : ev) <= q) j = cand;
+        }
+        const uint32_t eja = __shfl_sync(0xFFFFFFFFu, xa, j), ejv = __shfl_sync(0xFFFFFFFFu, xv, j);
+        const uint32_t ej = is_a ? eja : ejv;
+        if (e < ta + tv) {
+          const uint32_t id = pm[(is_a ? 0u : 16u * kMbox) + j * kMbox + (q - ej)];
+          if (is_a) {
+            const uint32_t pos = atomicAdd(&ctl->fpos_a, 1u);
+            c.aring[pos & c.amask] = id;
+            atomicAdd(&cur->afree, 1u);
+          } else {
+            const uint32_t pos = atomicAdd(&ctl->fpos_v, 1u);
+            c.vring[pos & c.vmask] = id;
+            atomicAdd(&cur->vfree, 1u);
+          }
+        }
+      }
     }
     // CTA k takes the pairs whose global index is k mod G: an even sample of
     // every CTA's queue.
@@ -1317,9 +1445,10 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
         if (v && !act && !c.failed) link(c, eq.x, eq.y);
       }
     } else {
-      const uint2* in = lqueue + ((r - 1) & 1u) * cap_q;
-      for (uint32_t mb = threadIdx.x & ~31u; rank + G * mb < N; mb += kBlock) {
-        const uint32_t i = rank + G * (mb + lane);
+      // this CTA's pairs: producer j dealt it n_j of them, in slots [0, n_j) of queue j
+      const uint2* in = lqueue + ((r - 1) & 1u) * 16 * cap_q;
+      for (uint32_t mb = threadIdx.x & ~31u; mb < N; mb += kBlock) {
+        const uint32_t i = mb + lane;
         // segment j of global index i: the last j with excl_j <= i
         uint32_t j = 0;
 #pragma unroll
@@ -1331,13 +1460,13 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
         const uint32_t ej = __shfl_sync(0xFFFFFFFFu, excl, j);
         const bool v = i < N && !c.failed;
         INET_TR(c, 0);
-        const uint2 e = v ? dsmem_ld2(in + (i - ej), j) : make_uint2(0, 0);
+        const uint2 e = v ? in[j * cap_q + (i - ej)] : make_uint2(0, 0);
         interact_w(c, v, e.x, e.y);
         if (v) {
 #ifdef INET_TRACE
           {
             const long long t6 = clock64();
-            if (atomicAdd(&inet_trace_count, 1u) < 400u)
+            if (r >= INET_TRACE_R0 && r < INET_TRACE_R0 + 2 && atomicAdd(&inet_trace_count, 1u) < 1200u)
               printf("TR r=%u k=%u t=%u q+ag=%lld pair=%lld alloc=%lld wr+free=%lld exch=%lld settle=%lld\n", r, rank,
                      threadIdx.x, c.tr[2] - c.tr[0], c.tr[2] - c.tr[1], c.tr[3] - c.tr[2], c.tr[4] - c.tr[3],
                      c.tr[5] - c.tr[4], t6 - c.tr[5]);
@@ -1359,19 +1488,29 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     }
     // every CTA pushes its round counters into every CTA's inbox
     __syncthreads();
-    if (threadIdx.x < G)
-      dsmem_st4(&inbox[(r % 3) * 16 + rank], threadIdx.x,
-                make_uint4(cur->qcount, cur->ints, cur->comms, static_cast<uint32_t>(cur->parked)));
+    if (threadIdx.x < G) {
+      const uint32_t k = threadIdx.x;
+      uint4* dst = &inbox[(r % 3) * 32 + 2 * rank];
+      dsmem_st4(dst, k, make_uint4(cur->qcount, cur->ints, cur->comms, static_cast<uint32_t>(cur->parked)));
+      dsmem_st4(dst + 1, k, make_uint4(c.outc[k], c.outc[16 + k], 0u, 0u));
+    }
     CT_MARK(2);
     cluster_barrier();
     CT_MARK(3);
     // ---- round r is closed on every CTA: its counters are in the local inbox
     uint4 w = make_uint4(0, 0, 0, 0);
-    if (lane < G) w = inbox[(r % 3) * 16 + lane];
+    if (lane < G) w = inbox[(r % 3) * 32 + 2 * lane];
     const bool err_any = __any_sync(0xFFFFFFFFu, (w.x & kErrBit) != 0);
     w.x &= ~kErrBit;
-    uint32_t total;
-    excl = warp_excl_scan(w.x, lane, total);
+    uint32_t total;  // pairs queued cluster-wide
+    warp_excl_scan(w.x, lane, total);
+    // pairs producer `lane` dealt to this CTA: its p-th went to CTA (p + lane) mod G
+    uint32_t mine;
+    {
+      const uint32_t dd = (rank - lane) & (G - 1);
+      const uint32_t nj = lane < G && w.x > dd ? ((w.x - dd - 1) >> c.gshift) + 1 : 0u;
+      excl = warp_excl_scan(nj, lane, mine);
+    }
     {
       // ids freed to this CTA in round r become allocatable (nothing is dropped)
       const uint32_t atake = cur->atake, afree = cur->afree, vtake = cur->vtake, vfree = cur->vfree;
@@ -1405,7 +1544,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     }
     CT_MARK(0);
     rounds = r + 1;
-    N = total;
+    N = mine;
     if (err_any) {
       stop = true;
     } else if (total == 0) {

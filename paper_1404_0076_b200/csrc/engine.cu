@@ -362,7 +362,7 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
 
 // CTA size of tier C (one CTA per SM of the cluster).
 uint32_t cluster_threads(const inet_cfg* cfg) {
-  const uint32_t t = cfg && cfg->threads ? cfg->threads : 512;
+  const uint32_t t = cfg && cfg->threads ? cfg->threads : 256;
   if (t <= 64) return 64;
   if (t <= 128) return 128;
   if (t <= 256) return 256;
@@ -522,14 +522,16 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   // Large single nets: a cluster of G CTAs sharing their shared memory (tier C).
   // Its arenas are fixed by shared memory; a net that outgrows them falls
   // through to the single-CTA tiers.
-  const uint32_t want_g = cfg ? cfg->ctas_per_net : 0;
+  // auto (0): a single net takes a 16-CTA cluster; 1 forces one CTA per net
+  uint32_t want_g = cfg ? cfg->ctas_per_net : 0;
+  if (want_g == 0 && c->n_nets == 1 && !user_caps) want_g = 16;
   if (!done && want_g >= 2 && c->n_nets <= 64) {
     uint32_t G = 2;  // a power of two (ids are owned round-robin: owner = id & (G - 1))
     while (G * 2 <= std::min<uint32_t>(want_g, 16)) G *= 2;
     Shape sh = base_shape(c, max_loops);
     sh.res_agents = 4096;
     sh.res_vars = 4096;
-    sh.res_queue = 4096;
+    sh.res_queue = 256;  // pairs one CTA can deal to one CTA per round
     sh.ring_a = 4096;
     sh.ring_v = 4096;
     c->cluster_g = G;

@@ -87,6 +87,27 @@ __global__ void kern(int mode, int iters, uint32_t* gbuf, long long* out) {
         acc += __shfl_sync(~0u, v, 31);
         break;
       }
+      case 12: {  // 8 dependent local ATOMS by thread 0 (others idle at the barrier)
+        if (threadIdx.x == 0) for (int k = 0; k < 8; ++k) idx = atomicAdd(&ctr[idx & 3], 1u) & 0xFFFF;
+        bar_rel_acq();
+        break;
+      }
+      case 13: {  // same, while warps 1.. hammer remote DSMEM with loads
+        if (threadIdx.x == 0) for (int k = 0; k < 8; ++k) idx = atomicAdd(&ctr[idx & 3], 1u) & 0xFFFF;
+        else if (threadIdx.x >= 32) for (int k = 0; k < 8; ++k) acc += dsmem_ld(&ctr[(acc + k) & 3], (rank + 1 + k) % gridDim.x);
+        bar_rel_acq();
+        break;
+      }
+      case 14: {  // 8 dependent local ATOMS by lane 0 of every warp, same address
+        if (lane == 0) for (int k = 0; k < 8; ++k) idx = atomicAdd(&ctr[0], 1u) & 0xFFFF;
+        bar_rel_acq();
+        break;
+      }
+      case 15: {  // 8 dependent LDS by thread 0
+        if (threadIdx.x == 0) for (int k = 0; k < 8; ++k) idx = ctr[idx & 3] & 0xFFFF;
+        bar_rel_acq();
+        break;
+      }
       case 7: {  // dependent chain of 4 L2 loads per round by lane 0 of each warp
         bar_rel_acq();
         if (lane == 0) for (int k = 0; k < 4; ++k) { idx = gbuf[(idx + threadIdx.x) & 0xFFFF] & 0xFFFF; }
@@ -110,8 +131,11 @@ int main() {
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const char* names[] = {"barrier rel/acq", "barrier relaxed", "barrier+dsmem gather", "barrier+L2 load",
                          "barrier+atomicExch", "st.global+barrier", "__syncthreads", "barrier+4 dep L2 loads",
-                         "barrier+dsmem load", "barrier+4 dep dsmem loads", "barrier+dsmem exch", "push counts+barrier"};
-  for (int G : {2, 8, 16}) for (int T : {256, 512}) for (int mode = 0; mode < 12; ++mode) {
+                         "barrier+dsmem load", "barrier+4 dep dsmem loads", "barrier+dsmem exch", "push counts+barrier",
+                         "8 dep ATOMS + barrier", "8 dep ATOMS w/ DSMEM load + bar", "8 dep ATOMS all warps + bar",
+                         "8 dep LDS + barrier"};
+  for (int G : {1, 16}) for (int T : {256, 512}) for (int mode = 0; mode < 16; ++mode) {
+    if (G == 1 && (mode == 2 || mode == 8 || mode == 9 || mode == 10 || mode == 11 || mode == 13)) continue;
     cudaLaunchConfig_t lc{}; lc.gridDim = dim3(G); lc.blockDim = dim3(T); lc.dynamicSmemBytes = 0;
     cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension; at[0].val.clusterDim.x = G;
     at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1; lc.attrs = at; lc.numAttrs = 1;
