@@ -64,6 +64,7 @@ enum : int { kTierS = 0, kTierM = 1, kTierG = 2, kTierC = 3 };
 template <int kTier>
 struct Traits {
   using Ring = uint16_t;
+  static constexpr bool kCompact = kTier == kTierS;   // 8-byte agents with 16-bit refs in shared memory
   static constexpr bool kEnvSmem = false;           // per-thread source table in shared memory
   static constexpr bool kEnvLocal = kTier == kTierS;  // per-thread source table in local memory (L1)
   static constexpr bool kAgentsSmem = kTier == kTierS;
@@ -73,6 +74,7 @@ struct Traits {
 template <>
 struct Traits<kTierG> {
   using Ring = uint32_t;
+  static constexpr bool kCompact = false;
   static constexpr bool kEnvSmem = false;
   static constexpr bool kEnvLocal = false;
   static constexpr bool kAgentsSmem = false;
@@ -378,14 +380,32 @@ __device__ __forceinline__ uint32_t dsmem_exch(const void* p, uint32_t rank, uin
   return old;
 }
 
+// Tier S keeps agents as 8 bytes {label, p0 | p1, p2} with 16-bit refs
+// (bit 15 = variable, 0xFFFF = none; its arenas hold < 32768 ids), which
+// fits more nets per SM.
+__device__ __forceinline__ uint32_t ref16(uint32_t r) {
+  return r == kNone ? 0xFFFFu : ((r & kVar) ? (0x8000u | (r & 0x7FFFu)) : (r & 0x7FFFu));
+}
+__device__ __forceinline__ uint32_t ref32(uint32_t h) {
+  return h == 0xFFFFu ? kNone : ((h & 0x8000u) ? (kVar | (h & 0x7FFFu)) : h);
+}
+__device__ __forceinline__ uint2 pack_agent(const uint4& v) {
+  return make_uint2(v.x | (ref16(v.y) << 16), ref16(v.z) | (ref16(v.w) << 16));
+}
+__device__ __forceinline__ uint4 unpack_agent(const uint2& w) {
+  return make_uint4(w.x & 0xFFFFu, ref32(w.x >> 16), ref32(w.y & 0xFFFFu), ref32(w.y >> 16));
+}
+
 template <int kTier>
 __device__ __forceinline__ uint4 ld_agent(const Round<kTier>& c, uint32_t a) {
   if constexpr (kTier == kTierC) return dsmem_ld4(c.agents + (a >> c.gshift), a & (c.stride - 1));
+  else if constexpr (Traits<kTier>::kCompact) return unpack_agent(reinterpret_cast<const uint2*>(c.agents)[a]);
   else return c.agents[a];
 }
 template <int kTier>
 __device__ __forceinline__ void st_agent(const Round<kTier>& c, uint32_t a, const uint4& v) {
   if constexpr (kTier == kTierC) dsmem_st4(c.agents + (a >> c.gshift), a & (c.stride - 1), v);
+  else if constexpr (Traits<kTier>::kCompact) reinterpret_cast<uint2*>(c.agents)[a] = pack_agent(v);
   else c.agents[a] = v;
 }
 template <int kTier>
@@ -938,7 +958,7 @@ __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
     p.words = p.cagent_off + 4 * sh.res_agents;
     return p;
   }
-  p.slots_off = p.agents_off + (tier == kTierS ? 4 * sh.res_agents : 0);
+  p.slots_off = p.agents_off + (tier == kTierS ? 2 * sh.res_agents : 0);  // compact 8-byte agents
   const bool res_slots = tier != kTierG;
   p.queue_off = p.slots_off + (res_slots ? align4(sh.res_vars) : 0);
   p.env_off = p.queue_off + (res_slots ? align4(2 * sh.res_queue) : 0);
@@ -993,7 +1013,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   const bool fits = d.n_in_agents <= c.cap_agents && d.n_in_vars <= c.cap_vars;
   for (uint32_t i = threadIdx.x; i < c.cap_vars; i += blockDim.x) c.vslot[i] = kNone;
   if (fits)
-    for (uint32_t i = threadIdx.x; i < d.n_in_agents; i += blockDim.x) c.agents[i] = d.in_agents[i];
+    for (uint32_t i = threadIdx.x; i < d.n_in_agents; i += blockDim.x) st_agent(c, i, d.in_agents[i]);
   {
     uint32_t* w = reinterpret_cast<uint32_t*>(ctl);
     for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += blockDim.x) w[i] = 0;
@@ -1184,7 +1204,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   const uint32_t ahw = min(ctl->agent_bump, c.cap_agents);
   if constexpr (T::kAgentsSmem) {
     const uint32_t n_copy = min(ahw, d.cap_agents);
-    for (uint32_t i = threadIdx.x; i < n_copy; i += blockDim.x) d.agents[i] = c.agents[i];
+    for (uint32_t i = threadIdx.x; i < n_copy; i += blockDim.x) d.agents[i] = ld_agent(c, i);
   }
   if (threadIdx.x == 0) {
     NetCtl* g = d.ctl;
