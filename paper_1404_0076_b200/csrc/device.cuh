@@ -334,9 +334,10 @@ __device__ __forceinline__ uint32_t dsmem_ld(const void* p, uint32_t rank) {
 // A CTA never owns more ids than its ring holds, so nothing is dropped.
 template <int kTier>
 __device__ __forceinline__ void free_owned(Round<kTier>& c, uint32_t id, uint32_t* fpos, uint32_t* ring, uint32_t mask,
-                                           uint32_t* cnt, uint32_t* outc, uint32_t* mbox) {
+                                           uint32_t* cnt, uint32_t* outc, uint32_t* mbox, uint32_t* slots) {
   const uint32_t k = id & (c.stride - 1);
   if (k == c.rank) {
+    if (slots) slots[id >> c.gshift] = kNone;  // a dead variable's slot, cleared by its owner
     const uint32_t pos = atomicAdd(fpos, 1u);
     ring[pos & mask] = id;
     atomicAdd(cnt, 1u);
@@ -354,6 +355,7 @@ __device__ __forceinline__ void free_owned(Round<kTier>& c, uint32_t id, uint32_
     return;
   }
   const uint32_t pos = dsmem_atom_add(fpos, k, 1u);  // mailbox full: straight into the owner's ring
+  if (slots) dsmem_st(&slots[id >> c.gshift], k, kNone);
   dsmem_st(&ring[pos & mask], k, id);
   dsmem_red_add(cnt, k, 1u);
 }
@@ -460,7 +462,8 @@ __device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, Claim&
 template <int kTier>
 __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
   if constexpr (kTier == kTierC) {
-    free_owned(c, a, &c.ctl->fpos_a, reinterpret_cast<uint32_t*>(c.aring), c.amask, &c.cur->afree, c.outc, c.mbox_a);
+    free_owned(c, a, &c.ctl->fpos_a, reinterpret_cast<uint32_t*>(c.aring), c.amask, &c.cur->afree, c.outc, c.mbox_a,
+               static_cast<uint32_t*>(nullptr));
     return;
   }
   const uint32_t f = atomicAdd(&c.cur->afree, 1u);
@@ -472,7 +475,7 @@ template <int kTier>
 __device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
   if constexpr (kTier == kTierC) {
     free_owned(c, x, &c.ctl->fpos_v, reinterpret_cast<uint32_t*>(c.vring), c.vmask, &c.cur->vfree, c.outc + 16,
-               c.mbox_v);
+               c.mbox_v, c.vslot);
     return;
   }
   const uint32_t f = atomicAdd(&c.cur->vfree, 1u);
@@ -558,7 +561,9 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
       c.parked += 1;
       return;
     }
-    st_slot(c, x, kNone);  // x is dead: both occurrences met
+    // x is dead: both occurrences met. Tier C leaves the slot to its owner,
+    // which clears it locally when the id comes back to its ring (no remote store).
+    if constexpr (kTier != kTierC) st_slot(c, x, kNone);
     c.comms += 1;
     c.parked -= 1;
     free_var(c, x);
@@ -702,9 +707,14 @@ template <uint32_t MF, uint32_t MX, int kTier>
 __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uint32_t nx, uint32_t (&f)[MF],
                                                uint32_t (&g)[MX]) {
   if ((nf | nx) == 0) return true;
+  INET_TR(c, 6);
   const uint32_t tv = nf ? atomicAdd(&c.cur->vtake, nf) : 0u;
   const uint32_t ta = nx ? atomicAdd(&c.cur->atake, nx) : 0u;
   const uint32_t av_v = c.hi_v - c.lo_v, av_a = c.hi_a - c.lo_a;
+#ifdef INET_TRACE
+  if ((tv | ta) == 0xFFFFFFFFu) c.tr[7] = 0;
+  c.tr[7] = clock64();
+#endif
   const uint32_t gv = tv < av_v ? min(av_v - tv, nf) : 0u, ga = ta < av_a ? min(av_a - ta, nx) : 0u;
   uint32_t bv = 0, ba = 0;
   if (gv < nf) {
@@ -1445,6 +1455,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
             c.aring[pos & c.amask] = id;
             atomicAdd(&cur->afree, 1u);
           } else {
+            lslots[id >> c.gshift] = kNone;  // the variable died last round; its slot is ours to clear
             const uint32_t pos = atomicAdd(&ctl->fpos_v, 1u);
             c.vring[pos & c.vmask] = id;
             atomicAdd(&cur->vfree, 1u);
@@ -1479,6 +1490,9 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
         }
         const uint32_t ej = __shfl_sync(0xFFFFFFFFu, excl, j);
         const bool v = i < N && !c.failed;
+#ifdef INET_TRACE
+        c.tr[6] = c.tr[7] = 0;
+#endif
         INET_TR(c, 0);
         const uint2 e = v ? in[j * cap_q + (i - ej)] : make_uint2(0, 0);
         interact_w(c, v, e.x, e.y);
@@ -1486,10 +1500,11 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
 #ifdef INET_TRACE
           {
             const long long t6 = clock64();
-            if (r >= INET_TRACE_R0 && r < INET_TRACE_R0 + 2 && atomicAdd(&inet_trace_count, 1u) < 1200u)
-              printf("TR r=%u k=%u t=%u q+ag=%lld pair=%lld alloc=%lld wr+free=%lld exch=%lld settle=%lld\n", r, rank,
-                     threadIdx.x, c.tr[2] - c.tr[0], c.tr[2] - c.tr[1], c.tr[3] - c.tr[2], c.tr[4] - c.tr[3],
-                     c.tr[5] - c.tr[4], t6 - c.tr[5]);
+            if (r >= INET_TRACE_R0 && r < INET_TRACE_R0 + 2 && ((threadIdx.x & 31u) == 0 || (c.tr[6] != 0)) &&
+                atomicAdd(&inet_trace_count, 1u) < 1200u)
+              printf("TR r=%u k=%u t=%u q+ag=%lld pair=%lld alloc=%lld wr+free=%lld exch=%lld settle=%lld pre=%lld atoms=%lld\n",
+                     r, rank, threadIdx.x, c.tr[2] - c.tr[0], c.tr[2] - c.tr[1], c.tr[3] - c.tr[2], c.tr[4] - c.tr[3],
+                     c.tr[5] - c.tr[4], t6 - c.tr[5], c.tr[6] - c.tr[2], c.tr[7] - c.tr[6]);
           }
 #endif
         }
@@ -1597,6 +1612,16 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   e_code = __shfl_sync(0xFFFFFFFFu, e_code, e_src);
   e_a = __shfl_sync(0xFFFFFFFFu, e_a, e_src);
   e_b = __shfl_sync(0xFFFFFFFFu, e_b, e_src);
+  // variables that died in the last round and were mailed here: clear their slots
+  if (!stop_err && rounds >= 2) {
+    const uint32_t rl = rounds - 1;
+    const uint32_t* pm = mbox + (rl & 1u) * 2 * 16 * kMbox + 16 * kMbox;
+    for (uint32_t e = threadIdx.x; e < 16 * kMbox; e += kBlock) {
+      const uint32_t src = e / kMbox, q = e % kMbox;
+      if (src < G && q < min(inbox[(rl % 3) * 32 + 2 * src + 1].y, kMbox)) lslots[pm[e] >> c.gshift] = kNone;
+    }
+    __syncthreads();
+  }
   // write this CTA's share of the agents and slots back to the global arrays
   {
     const uint32_t na = min(ctl->agent_bump, c.cap_agents), nv = min(ctl->var_bump, c.cap_vars);
