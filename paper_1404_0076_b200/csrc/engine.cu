@@ -116,6 +116,41 @@ struct DevBuf {
   }
 };
 
+// Page-locked host buffer (grow-only): result copies run at full PCIe/C2C speed.
+struct PinnedU32 {
+  uint32_t* p = nullptr;
+  size_t n = 0, cap = 0;
+  bool pinned = false;
+  void release() {
+    if (p) {
+      if (pinned)
+        cudaFreeHost(p);
+      else
+        std::free(p);
+    }
+    p = nullptr;
+    cap = 0;
+  }
+  ~PinnedU32() { release(); }
+  void resize(size_t want) {
+    if (want > cap) {
+      release();
+      const size_t bytes = std::max<size_t>(want, 1) * 4;
+      pinned = cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocDefault) == cudaSuccess;
+      if (!pinned) {
+        cudaGetLastError();
+        p = static_cast<uint32_t*>(std::malloc(bytes));  // plain memory still works, just slower
+      }
+      cap = want;
+    }
+    n = want;
+  }
+  uint32_t* data() { return p; }
+  const uint32_t* data() const { return p; }
+  bool empty() const { return n == 0; }
+  size_t size() const { return n; }
+};
+
 struct inet_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -144,8 +179,8 @@ struct inet_ctx {
   // results (host)
   std::vector<NetCtl> ctl;
   std::vector<inet_net_stats> stats;
-  std::vector<uint32_t> h_agents;     // per-net slab prefixes [n_nets * agent_pitch * 4]
-  std::vector<uint32_t> h_resid;      // [n_nets * resid_pitch * 2]
+  PinnedU32 h_agents;                 // per-net slab prefixes [n_nets * agent_pitch * 4]
+  PinnedU32 h_resid;                  // [n_nets * resid_pitch * 2]
   uint32_t agent_pitch = 0, resid_pitch = 0;
   std::vector<uint32_t> h_rounds;     // [n_nets * cap_rounds * 4]
   std::vector<inethost::NormalForm> results;

@@ -18,7 +18,6 @@
 
 #include <algorithm>
 #include <atomic>
-#include <deque>
 #include <thread>
 
 namespace inethost {
@@ -43,6 +42,7 @@ struct Finalizer {
   std::vector<uint32_t> owner;   // container of each agent
   std::vector<uint32_t> parent;  // union-find over containers [0, ni+ne)
   std::vector<uint8_t> alive;
+  std::vector<uint32_t> fifo;
 
   uint32_t eq_cell(uint32_t e, uint32_t s) const { return ni + 2 * e + s; }
   uint32_t port_cell(uint32_t a, uint32_t k) const { return ni + 2 * ne + 3 * a + k; }
@@ -68,8 +68,11 @@ struct Finalizer {
   }
 
   // Record occurrences and owners below one root cell.
+  std::vector<uint32_t> stack;  // scan work list, reused across roots
+
   int scan(uint32_t root_cell, uint32_t container) {
-    std::vector<uint32_t> stack{root_cell};
+    stack.clear();
+    stack.push_back(root_cell);
     while (!stack.empty()) {
       const uint32_t c = stack.back();
       stack.pop_back();
@@ -107,11 +110,12 @@ struct Finalizer {
       for (uint32_t s = 0; s < 2; ++s)
         if (int st = scan(eq_cell(e, s), ni + e)) return st;
 
-    std::deque<uint32_t> queue;
+    // FIFO of equations to visit (the reference's queue discipline)
+    std::vector<uint32_t>& queue = fifo;
+    queue.clear();
     for (uint32_t e = 0; e < ne; ++e) queue.push_back(e);
-    while (!queue.empty()) {
-      const uint32_t e = queue.front();
-      queue.pop_front();
+    for (size_t head = 0; head < queue.size();) {
+      const uint32_t e = queue[head++];
       if (!alive[e]) continue;
       for (uint32_t side = 0; side < 2; ++side) {
         const uint32_t v = eq[2 * e + side];
@@ -189,7 +193,14 @@ int validate_rule_blob(const uint32_t* blob, size_t n_words) {
 
 int finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface, uint32_t* eqs,
                   uint32_t n_eqs, uint32_t n_vars, uint8_t* alive) {
-  Finalizer f{agents, n_agents, iface, n_iface, eqs, n_eqs, n_vars, {}, {}, {}, {}};
+  Finalizer f{};
+  f.ag = agents;
+  f.na = n_agents;
+  f.ifc = iface;
+  f.ni = n_iface;
+  f.eq = eqs;
+  f.ne = n_eqs;
+  f.nv = n_vars;
   int st = f.run();
   if (st) return st;
   if (alive) std::copy(f.alive.begin(), f.alive.end(), alive);
@@ -197,16 +208,36 @@ int finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t
 }
 
 int finalize_net(const NetView& v, NormalForm& out) {
-  std::vector<uint32_t> ag(v.agents, v.agents + size_t(v.n_agents) * 4);
-  std::vector<uint32_t> ifc(v.iface, v.iface + v.n_iface);
-  std::vector<uint32_t> eq(v.residual, v.residual + size_t(v.n_residual) * 2);
-  Finalizer f{ag.data(), v.n_agents, ifc.data(), v.n_iface, eq.data(), v.n_residual, v.n_vars, {}, {}, {}, {}};
+  // per-thread scratch, reused across the nets a worker finalizes (a batch of
+  // 4096 nets would otherwise spend most of its time in the allocator)
+  struct Scratch {
+    std::vector<uint32_t> ag, ifc, eq, remap, order, stack;
+    Finalizer f{};
+  };
+  thread_local Scratch sc;
+  std::vector<uint32_t>& ag = sc.ag;
+  std::vector<uint32_t>& ifc = sc.ifc;
+  std::vector<uint32_t>& eq = sc.eq;
+  ag.assign(v.agents, v.agents + size_t(v.n_agents) * 4);
+  ifc.assign(v.iface, v.iface + v.n_iface);
+  eq.assign(v.residual, v.residual + size_t(v.n_residual) * 2);
+  Finalizer& f = sc.f;
+  f.ag = ag.data();
+  f.na = v.n_agents;
+  f.ifc = ifc.data();
+  f.ni = v.n_iface;
+  f.eq = eq.data();
+  f.ne = v.n_residual;
+  f.nv = v.n_vars;
   int st = f.run();
   if (st) return st;
   // compact the reachable normal form in preorder
-  std::vector<uint32_t> remap(v.n_agents, kNone);
-  std::vector<uint32_t> order;
-  std::vector<uint32_t> stack;
+  std::vector<uint32_t>& remap = sc.remap;
+  std::vector<uint32_t>& order = sc.order;
+  std::vector<uint32_t>& stack = sc.stack;
+  remap.assign(v.n_agents, kNone);
+  order.clear();
+  stack.clear();
   auto visit = [&](uint32_t root) {
     if (root == kNone || (root & kVar)) return;
     stack.push_back(root);
