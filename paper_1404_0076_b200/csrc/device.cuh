@@ -731,14 +731,17 @@ __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uin
       return false;
     }
   }
+  // ring entries loaded unconditionally (masked indices are always in range) so
+  // the loads issue back to back instead of one predicated block per id
+  uint32_t rv[MF], ra[MX];
 #pragma unroll
-  for (uint32_t j = 0; j < MF; ++j)
-    if (j < nf)
-      f[j] = kVar | (j < gv ? static_cast<uint32_t>(c.vring[(c.lo_v + tv + j) & c.vmask]) : bump_var(c, bv + (j - gv)));
+  for (uint32_t j = 0; j < MF; ++j) rv[j] = c.vring[(c.lo_v + tv + j) & c.vmask];
 #pragma unroll
-  for (uint32_t j = 0; j < MX; ++j)
-    if (j < nx)
-      g[j] = j < ga ? static_cast<uint32_t>(c.aring[(c.lo_a + ta + j) & c.amask]) : bump_agent(c, ba + (j - ga));
+  for (uint32_t j = 0; j < MX; ++j) ra[j] = c.aring[(c.lo_a + ta + j) & c.amask];
+#pragma unroll
+  for (uint32_t j = 0; j < MF; ++j) f[j] = kVar | (j < gv ? rv[j] : bump_var(c, bv + (j - gv)));
+#pragma unroll
+  for (uint32_t j = 0; j < MX; ++j) g[j] = j < ga ? ra[j] : bump_agent(c, ba + (j - ga));
   return true;
 }
 
