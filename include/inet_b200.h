@@ -93,6 +93,10 @@ typedef struct inet_cfg {
   uint32_t cap_vars;      /* initial per-net variable table; 0 = auto (grows on overflow) */
   uint32_t max_retries;   /* arena doublings before INET_ERR_ARENA; 0 = default */
   uint32_t count_rules;   /* per-rule interaction histogram (accounting runs only) */
+  uint32_t exact_loops;   /* 1: reference loop semantics — an equation a merge leaves var-headed
+                             communicates in the next round (engine.py:137-166), so rounds and
+                             LoopStats rows are the reference's loops; 0: link to a fixpoint
+                             within the round (fewer rounds) */
 } inet_cfg;
 
 /* Per-net outcome. */

@@ -52,6 +52,7 @@ class Cfg(C.Structure):
         ("cap_vars", C.c_uint32),
         ("max_retries", C.c_uint32),
         ("count_rules", C.c_uint32),
+        ("exact_loops", C.c_uint32),
     ]
 
 

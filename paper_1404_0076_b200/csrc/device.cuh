@@ -99,7 +99,8 @@ struct RoundCtr {
   uint32_t afree;   // agents offered to the ring
   uint32_t vtake;
   uint32_t vfree;
-  uint32_t pad[4];
+  uint32_t dcount;  // merged equations deferred to the next round (reference loop mode)
+  uint32_t pad[3];
 };
 
 // Parameters of the next round, written by the last warp to finish a round
@@ -108,7 +109,8 @@ struct Header {
   uint32_t n;       // active pairs in the queue
   uint32_t stop;    // leave the loop
   uint32_t lo_a, hi_a, lo_v, hi_v;  // ring windows allocatable in this round
-  uint32_t pad[2];
+  uint32_t nd;      // deferred equations to link first (reference loop mode)
+  uint32_t pad;
 };
 
 // Shared-memory control block of the net a CTA is reducing.
@@ -168,6 +170,10 @@ struct NetDesc {
   const uint4* in_agents;
   const uint2* in_eqs;
   uint32_t n_in_agents, n_in_eqs, n_in_vars, pad;
+  // reference loop mode: equations a merge left var-headed wait for the next
+  // round's communication, [2 parities][cap_def] (tier C: [2][G][cap_def / G])
+  uint2* deferred;
+  uint32_t cap_def, pad2;
 };
 
 // Launch-wide shape: ring sizes and the shared-memory capacities.
@@ -180,7 +186,7 @@ struct Shape {
   uint32_t rule_words;            // pair table + rule records (words)
   uint32_t n_labels;
   uint32_t threads;               // CTA size
-  uint32_t pad;
+  uint32_t exact;                 // 1: reference loop mode (merged var-headed equations wait a round)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -240,6 +246,8 @@ struct Round {
   uint32_t lo_a, hi_a, lo_v, hi_v;  // ring windows available this round
   uint32_t a_base, v_base, stride;  // tier C: bump sequence s -> id base + stride * s
   uint32_t rank, gshift;            // tier C: this CTA's rank in the cluster, log2 G
+  uint2* dout;                      // reference loop mode: this round's deferred equations (null: fixpoint)
+  uint32_t cap_def;
   uint32_t* outc;                   // tier C: ids mailed this round per owner: agents [0,16), vars [16,32)
   uint32_t* mbox_a;                 // tier C: mailboxes of this round, [src][kMbox] (owner's layout)
   uint32_t* mbox_v;
@@ -570,6 +578,18 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
     const uint32_t l = old, r = val;
     if (((l | r) & kVar) == 0) {
       push_active(c, l, r);
+      return;
+    }
+    if (c.dout) {
+      // reference loop mode: the merged equation communicates next round, as
+      // it would in the reference's next communication_phase (engine.py:137-166)
+      const uint32_t p = atomicAdd(&c.cur->dcount, 1u);
+      if (p >= c.cap_def) {
+        fail(c, INET_ERR_ARENA, 3);
+        return;
+      }
+      c.dout[p] = make_uint2(l, r);
+      c.parked += 1;  // live until linked
       return;
     }
     uint32_t key;
@@ -1060,6 +1080,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
 #endif
   const uint32_t n_warps = (blockDim.x + 31u) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
+  c.cap_def = d.cap_def;
   for (uint32_t r = 1;; ++r) {
     const Header h = ctl->hdr;
     if (h.stop) break;
@@ -1070,6 +1091,19 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     c.hi_v = h.hi_v;
     c.ints = c.comms = 0;
     c.parked = 0;
+    c.dout = sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
+    c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + (r & 1u) * qstride)
+                       : static_cast<void*>(static_cast<uint2*>(q0) + (r & 1u) * qstride);
+    if (h.nd) {
+      // equations merged last round that are still var-headed: this round's
+      // communication links them (reference loop mode)
+      const uint2* din = d.deferred + ((r - 1) & 1u) * d.cap_def;
+      for (uint32_t i = threadIdx.x; i < h.nd && !c.failed; i += blockDim.x) {
+        const uint2 eq = din[i];
+        c.parked -= 1;
+        link(c, eq.x, eq.y);
+      }
+    }
     if (r == 1) {
       // the input equations, in any class (communication_phase's first pass)
       c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + qstride)
@@ -1153,7 +1187,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
         for (int i = 0; i < static_cast<int>(sizeof(RoundCtr) / 4); ++i) dst[i] = src[i];
       }
       Header nh;
-      nh.pad[0] = nh.pad[1] = 0;
+      nh.pad = 0;
       // frees of round r were kept while they fit the ring (against its old window)
       const uint32_t wa = min(k.afree, sh.ring_a - (h.hi_a - h.lo_a));
       const uint32_t wv = min(k.vfree, sh.ring_v - (h.hi_v - h.lo_v));
@@ -1164,6 +1198,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       const bool round_failed = (k.qcount & kErrBit) != 0;
       k.qcount &= ~kErrBit;
       nh.n = k.qcount;
+      nh.nd = k.dcount;
       nh.stop = 0;
       const int32_t parked = ctl->parked_total + k.parked;
       ctl->parked_total = parked;
@@ -1181,7 +1216,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       ctl->rounds = r + 1;
       if (round_failed) {
         nh.stop = 1;
-      } else if (k.qcount == 0) {
+      } else if (k.qcount == 0 && k.dcount == 0) {
         // the trailing no-op loop the reference records (engine.py:222-223)
         nh.stop = 1;
         if (d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked), 0);
@@ -1367,6 +1402,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   const uint32_t cap_q = sh.res_queue;  // pairs one producer can deal to one consumer per round
   c.cap_queue = cap_q;
   c.qj = cap_q;
+  c.cap_def = d.cap_def / G;
   const long long clk0 = clock64();
   const unsigned long long gt0 = globaltimer();
   // ---- init: this CTA's share of the input agents, empty slots, zero counters
@@ -1421,6 +1457,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     c.ints = c.comms = 0;
     c.parked = 0;
     c.inq = lqueue + (r & 1u) * 16 * cap_q;
+    c.dout = sh.exact ? d.deferred + ((r & 1u) * G + rank) * c.cap_def : nullptr;
     c.outc = outc3 + (r % 3) * 32;
     c.mbox_a = mbox + (r & 1u) * 2 * 16 * kMbox;
     c.mbox_v = c.mbox_a + 16 * kMbox;
@@ -1466,8 +1503,16 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
         }
       }
     }
-    // CTA k takes the pairs whose global index is k mod G: an even sample of
-    // every CTA's queue.
+    if (r > 1 && sh.exact) {
+      // this CTA's equations merged last round that are still var-headed
+      const uint32_t nd = ctr3[(r - 1) % 3].dcount;
+      const uint2* din = d.deferred + (((r - 1) & 1u) * G + rank) * c.cap_def;
+      for (uint32_t i = threadIdx.x; i < nd && !c.failed; i += kBlock) {
+        const uint2 eq = din[i];
+        c.parked -= 1;
+        link(c, eq.x, eq.y);
+      }
+    }
     if (r == 1) {
       // the input equations, in any class (communication_phase's first pass)
       for (uint32_t mb = threadIdx.x & ~31u; rank + G * mb < N; mb += kBlock) {
@@ -1530,7 +1575,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
       const uint32_t k = threadIdx.x;
       uint4* dst = &inbox[(r % 3) * 32 + 2 * rank];
       dsmem_st4(dst, k, make_uint4(cur->qcount, cur->ints, cur->comms, static_cast<uint32_t>(cur->parked)));
-      dsmem_st4(dst + 1, k, make_uint4(c.outc[k], c.outc[16 + k], 0u, 0u));
+      dsmem_st4(dst + 1, k, make_uint4(c.outc[k], c.outc[16 + k], cur->dcount, 0u));
     }
     CT_MARK(2);
     cluster_barrier();
@@ -1542,6 +1587,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     w.x &= ~kErrBit;
     uint32_t total;  // pairs queued cluster-wide
     warp_excl_scan(w.x, lane, total);
+    const bool deferred_any = __any_sync(0xFFFFFFFFu, lane < G && inbox[(r % 3) * 32 + 2 * lane + 1].z != 0);
     // pairs producer `lane` dealt to this CTA: its p-th went to CTA (p + lane) mod G
     uint32_t mine;
     {
@@ -1575,7 +1621,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
             d.stats[r - 1] = make_uint4(ri, rc, total + static_cast<uint32_t>(parked_tot),
                                         static_cast<uint32_t>(now - t_prev));
           t_prev = now;
-          if (!err_any && total == 0 && r < d.cap_rounds)
+          if (!err_any && total == 0 && !deferred_any && r < d.cap_rounds)
             d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
         }
       }
@@ -1585,7 +1631,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     N = mine;
     if (err_any) {
       stop = true;
-    } else if (total == 0) {
+    } else if (total == 0 && !deferred_any) {
       stop = true;  // the trailing no-op loop the reference records (engine.py:222-223)
     } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
       stop = true;

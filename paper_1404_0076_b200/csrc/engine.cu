@@ -166,7 +166,9 @@ struct inet_ctx {
   uint32_t max_in_agents = 0, max_in_eqs = 0, max_in_vars = 0;
   bool input_resident = false;
   // device state
-  DevBuf d_in_agents, d_in_eqs, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist;
+  DevBuf d_in_agents, d_in_eqs, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist,
+      d_defer;
+  uint32_t cap_def = 0;  // deferred equations per net and round (reference loop mode)
   bool count_rules = false;
   std::vector<uint32_t> h_hist;
   uint64_t io_h2d = 0, io_d2h = 0;
@@ -255,7 +257,7 @@ void inet_ctx_destroy(inet_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->d_blob, &c->d_in_agents, &c->d_in_eqs, &c->d_desc, &c->d_agents, &c->d_vslot, &c->d_aring,
-                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist})
+                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer})
     b->release();
   for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -353,7 +355,8 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
       c->d_queue.ensure(N * 2 * cap_queue * 8) || c->d_resid.ensure(N * cap_vars * 8) ||
       c->d_ctl.ensure(N * sizeof(NetCtl)) || c->d_desc.ensure(N * sizeof(NetDesc)) ||
       (cap_rounds && c->d_stats.ensure(N * cap_rounds * 16)) ||
-      (c->count_rules && c->d_hist.ensure(N * hist_stride(c) * 4)))
+      (c->count_rules && c->d_hist.ensure(N * hist_stride(c) * 4)) ||
+      (c->cap_def && c->d_defer.ensure(N * 2 * c->cap_def * 8)))
     return INET_ERR_CUDA;
   if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * hist_stride(c) * 4, c->stream));
   std::vector<NetDesc> desc(n);
@@ -371,6 +374,8 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.cap_vars = cap_vars;
     d.cap_queue = cap_queue;
     d.cap_rounds = cap_rounds;
+    d.deferred = c->cap_def ? static_cast<uint2*>(c->d_defer.p) + size_t(i) * 2 * c->cap_def : nullptr;
+    d.cap_def = c->cap_def;
     d.in_agents = static_cast<const uint4*>(c->d_in_agents.p) + c->agent_off[i];
     d.in_eqs = static_cast<const uint2*>(c->d_in_eqs.p) + c->eq_off[i];
     d.n_in_agents = static_cast<uint32_t>(c->agent_off[i + 1] - c->agent_off[i]);
@@ -528,7 +533,14 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   bool done = false;
   // Try the shared-memory tiers first; a net that overflows sends the whole
   // launch to the next tier (S or M, then G with doubling capacities).
-  auto attempt_tier = [&](int tier, const Shape& sh, uint32_t ca, uint32_t cv, uint32_t cq) -> int {
+  const bool exact = cfg && cfg->exact_loops;
+  auto attempt_tier = [&](int tier, const Shape& sh0, uint32_t ca, uint32_t cv, uint32_t cq) -> int {
+    Shape sh = sh0;
+    sh.exact = exact ? 1u : 0u;
+    // deferred equations per round: the round's queue size is a safe bound in
+    // practice; an overflow reports ARENA and the next attempt grows it
+    c->cap_def = exact ? (tier == kTierC ? c->cluster_g * 1024u : std::max<uint32_t>(256u, tier == kTierG ? cq : sh.res_queue))
+                       : 0u;
     int st = layout(c, ca, cv, cq, cap_rounds);
     if (st) return st;
     st = launch(c, cfg, sh, tier, &ms);

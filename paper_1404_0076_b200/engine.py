@@ -47,7 +47,10 @@ class EngineConfig:
 
     ``worker_hint`` is accepted for compatibility; the device decides its own
     parallelism. ``device`` selects the GPU; ``threads`` the CTA size per net
-    (0 = auto).
+    (0 = auto); ``ctas_per_net`` the cluster size of a single net (0 = auto);
+    ``exact_loops`` keeps the reference's loop structure (a merged equation
+    that is still var-headed communicates in the next loop, so ``loops`` rows
+    are the reference's), False links to a fixpoint within a round.
     """
 
     slot_count: Optional[int] = None
@@ -58,6 +61,7 @@ class EngineConfig:
     device: int = 0
     threads: int = 0
     ctas_per_net: int = 0
+    exact_loops: bool = True
 
 
 @dataclass(slots=True)
@@ -200,6 +204,7 @@ def native_cfg(cfg: EngineConfig) -> _native.Cfg:
     k.collect_stats = 1 if cfg.collect_stats else 0
     k.threads = cfg.threads
     k.ctas_per_net = cfg.ctas_per_net
+    k.exact_loops = 1 if cfg.exact_loops else 0
     return k
 
 

@@ -262,3 +262,40 @@ def test_cluster_tier_random_arith_against_oracle():
         want = O.run_config(net, orules, collect=False)
         assert res.total_interactions == want.interactions
         assert print_configuration(res.final) == want.printed()
+
+
+# ---- reference loop mode: LoopStats rows are the reference's loops ----------
+
+# Rule sets whose right-hand sides never equate two variables. With var=var
+# equations the reference's loop timing depends on its own variable numbering
+# (the smaller id keys the equation, engine.py:150-153), which a parallel
+# allocator does not reproduce; interactions and normal forms never depend on it.
+NO_VAR_VAR = ("ackermann", "lsystem")
+
+
+@pytest.mark.parametrize("g", [1, 16])
+def test_loop_rows_equal_reference(g):
+    """exact_loops=True: loop count, per-loop interactions and live equations equal the
+    reference fixtures row for row (engine.py:215-221)."""
+    checked = 0
+    for case in CASES:
+        if case.get("program") not in NO_VAR_VAR or not case.get("loops"):
+            continue
+        config, rules = _case_inputs(case)
+        res = evaluate(config, rules, EngineConfig(ctas_per_net=g, exact_loops=True))
+        want = case["loops"]
+        got = [(s.interactions, s.live_equations) for s in res.loops]
+        assert len(got) == len(want), case["name"]
+        assert [w[0] for w in want] == [x[0] for x in got], case["name"]  # interactions per loop
+        assert [w[2] for w in want] == [x[1] for x in got], case["name"]  # live equations per loop
+        checked += 1
+    assert checked >= 10
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_both_loop_modes_reach_the_same_normal_form(exact):
+    prog = programs.program("fibonacci")
+    res = evaluate(prog.build_input(18), prog.rules, EngineConfig(exact_loops=exact))
+    assert res.total_interactions == 50_515
+    assert programs.nat_value(res.final.interface[0]) == 2584
+    _check_loops(res)
