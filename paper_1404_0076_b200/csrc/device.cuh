@@ -174,6 +174,12 @@ struct NetDesc {
   // round's communication, [2 parities][cap_def] (tier C: [2][G][cap_def / G])
   uint2* deferred;
   uint32_t cap_def, pad2;
+  // tier C resuming a net that tier M handed over (its arena, slot table and
+  // pending equations are the inputs): the rounds and totals already done
+  uint32_t resume, round_base;
+  unsigned long long base_ints, base_comms;
+  int32_t base_parked;
+  uint32_t pad3;
 };
 
 // Launch-wide shape: ring sizes and the shared-memory capacities.
@@ -187,7 +193,12 @@ struct Shape {
   uint32_t n_labels;
   uint32_t threads;               // CTA size
   uint32_t exact;                 // 1: reference loop mode (merged var-headed equations wait a round)
+  uint32_t promote_ints;          // tier M: give the net up to the cluster tier past this many interactions
+  uint32_t pad;
 };
+
+// Internal status of a single-CTA run that outgrew it (not returned to callers).
+constexpr uint32_t kPromote = 0x100u;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -1223,6 +1234,9 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
         nh.stop = 1;
         atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_LOOP_CAP));
+      } else if (sh.promote_ints && ctl->tot_i >= sh.promote_ints) {
+        nh.stop = 1;  // a large net: the host reruns it on a cluster
+        atomicCAS(&ctl->err_code, 0u, kPromote);
       }
       ctl->ctr = RoundCtr{};
       ctl->hdr = nh;
@@ -1241,7 +1255,23 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   // ---- results: residual parked equations in variable-id order, arena copy
   const uint32_t hw = min(ctl->var_bump, c.cap_vars);
   uint32_t base = 0;
-  for (uint32_t c0 = 0; c0 < hw; c0 += blockDim.x) {
+  const bool handed = kTier == kTierM && ctl->err_code == kPromote;
+  if constexpr (kTier == kTierM) {
+    if (handed) {
+      // handing the net over to a cluster (tier C resumes it): the slot table,
+      // then the next round's pairs followed by its deferred equations
+      const uint32_t r = ctl->rounds - 1, n = ctl->hdr.n, nd = ctl->hdr.nd;
+      for (uint32_t x = threadIdx.x; x < hw; x += blockDim.x) d.vslot[x] = c.vslot[x];
+      const uint32_t* pq = static_cast<const uint32_t*>(q0) + (r & 1u) * qstride;
+      const uint2* pd = d.deferred + (r & 1u) * d.cap_def;
+      for (uint32_t i = threadIdx.x; i < n + nd && i < d.cap_queue; i += blockDim.x)
+        d.queue[i] = i < n ? make_uint2(pq[i] >> 16, pq[i] & 0xFFFFu) : pd[i - n];
+      base = n + nd;
+      if (base > d.cap_queue && threadIdx.x == 0) ctl->err_code = INET_ERR_ARENA;
+      __syncthreads();
+    }
+  }
+  for (uint32_t c0 = 0; c0 < hw && !handed; c0 += blockDim.x) {
     const uint32_t x = c0 + threadIdx.x;
     const uint32_t v = x < hw ? c.vslot[x] : kNone;
     uint32_t off;
@@ -1408,7 +1438,8 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   // ---- init: this CTA's share of the input agents, empty slots, zero counters
   const bool fits = s0_a <= c.cap_agents && s0_v <= c.cap_vars && uint64_t(G) * c.cap_agents <= d.cap_agents &&
                     uint64_t(G) * c.cap_vars <= d.cap_vars;
-  for (uint32_t i = threadIdx.x; i < c.cap_vars; i += kBlock) lslots[i] = kNone;
+  for (uint32_t i = threadIdx.x; i < c.cap_vars; i += kBlock)
+    lslots[i] = d.resume && i < s0_v ? d.vslot[rank + G * i] : kNone;
   if (fits)
     for (uint32_t i = threadIdx.x; i < s0_a; i += kBlock) lagents[i] = d.in_agents[rank + G * i];
   {
@@ -1432,8 +1463,9 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   c.failed = false;
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0;
   // running totals: thread 0 of CTA 0
-  unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
-  int32_t parked_tot = 0;
+  unsigned long long tot_i = d.base_ints, tot_c = d.base_comms, t_prev = globaltimer();
+  int32_t parked_tot = d.base_parked;
+  const uint32_t rb = d.round_base;  // rounds done before this launch (resume)
   uint32_t N = d.n_in_eqs, excl = 0, rounds = 1, stop_err = 0;
   bool stop = false;
   const bool writer = rank == 0 && threadIdx.x == 0;
@@ -1521,7 +1553,10 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
         const uint2 eq = v ? d.in_eqs[i] : make_uint2(0, 0);
         const bool act = v && ((eq.x | eq.y) & kVar) == 0;
         interact_w(c, act, eq.x, eq.y);
-        if (v && !act && !c.failed) link(c, eq.x, eq.y);
+        if (v && !act && !c.failed) {
+          if (d.resume) c.parked -= 1;  // a handed-over deferred equation was counted live
+          link(c, eq.x, eq.y);
+        }
       }
     } else {
       // this CTA's pairs: producer j dealt it n_j of them, in slots [0, n_j) of queue j
@@ -1617,12 +1652,12 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
 #else
           const unsigned long long now = globaltimer();
 #endif
-          if (r - 1 < d.cap_rounds)
-            d.stats[r - 1] = make_uint4(ri, rc, total + static_cast<uint32_t>(parked_tot),
-                                        static_cast<uint32_t>(now - t_prev));
+          if (rb + r - 1 < d.cap_rounds)
+            d.stats[rb + r - 1] = make_uint4(ri, rc, total + static_cast<uint32_t>(parked_tot),
+                                             static_cast<uint32_t>(now - t_prev));
           t_prev = now;
-          if (!err_any && total == 0 && !deferred_any && r < d.cap_rounds)
-            d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
+          if (!err_any && total == 0 && !deferred_any && rb + r < d.cap_rounds)
+            d.stats[rb + r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
         }
       }
     }
@@ -1633,7 +1668,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
       stop = true;
     } else if (total == 0 && !deferred_any) {
       stop = true;  // the trailing no-op loop the reference records (engine.py:222-223)
-    } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
+    } else if (rb + r + 1 > sh.max_rounds) {  // engine.py:205-207
       stop = true;
       stop_err = INET_ERR_LOOP_CAP;
     }
@@ -1712,7 +1747,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     g->err = stop_err ? stop_err : e_code;
     g->err_a = stop_err ? 0 : e_a;
     g->err_b = stop_err ? 0 : e_b;
-    g->rounds = rounds;
+    g->rounds = rb + rounds;
     g->interactions = tot_i;
     g->communications = tot_c;
     g->n_residual = n_res;

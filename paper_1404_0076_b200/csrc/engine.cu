@@ -175,6 +175,20 @@ struct inet_ctx {
   uint32_t cap_agents = 0, cap_vars = 0, cap_queue = 0, cap_rounds = 0;
   int tier = kTierG;  // tier of the last successful run
   uint32_t cluster_g = 1;  // CTAs per net of the last run (tier C)
+  // a single net promoted from one CTA to a cluster: the tier M prefix that
+  // ran up to the promotion threshold (replayed by inet_batch_rerun)
+  bool promoted = false;
+  uint32_t promote_ints = 1u << 19;  // env INET_B200_PROMOTE overrides
+  // the state tier M handed over, applied to the next layout (tier C resumes from it)
+  struct Resume {
+    bool on = false;
+    uint32_t agents = 0, vars = 0, pending = 0, round_base = 0;
+    uint64_t ints = 0, comms = 0;
+    int32_t parked = 0;
+  } resume;
+  Shape promo_shape{};
+  uint32_t promo_cap_def = 0;
+  float promo_ms = 0;
   Shape shape{};
   bool collect_stats = false;
   bool reduced = false;
@@ -244,6 +258,7 @@ int inet_ctx_create(int device, inet_ctx** out) {
   c->device = device;
   if (const char* e = std::getenv("INET_B200_JIT")) c->jit_mode = std::atoi(e);
   if (const char* e = std::getenv("INET_B200_JITSTYLE")) c->jit_style = std::atoi(e);
+  if (const char* e = std::getenv("INET_B200_PROMOTE")) c->promote_ints = static_cast<uint32_t>(std::atol(e));
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
     delete c;
@@ -381,6 +396,19 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.n_in_agents = static_cast<uint32_t>(c->agent_off[i + 1] - c->agent_off[i]);
     d.n_in_eqs = static_cast<uint32_t>(c->eq_off[i + 1] - c->eq_off[i]);
     d.n_in_vars = c->n_vars[i];
+    if (c->resume.on && n == 1) {
+      // resume from tier M's hand-over: its arena, slot table and pending equations
+      d.in_agents = d.agents;
+      d.in_eqs = d.queue;
+      d.n_in_agents = c->resume.agents;
+      d.n_in_eqs = c->resume.pending;
+      d.n_in_vars = c->resume.vars;
+      d.resume = 1;
+      d.round_base = c->resume.round_base;
+      d.base_ints = c->resume.ints;
+      d.base_comms = c->resume.comms;
+      d.base_parked = c->resume.parked;
+    }
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_desc.p, desc.data(), N * sizeof(NetDesc), cudaMemcpyHostToDevice, c->stream));
   return INET_OK;
@@ -495,6 +523,24 @@ int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
   return INET_OK;
 }
 
+// Tier M runs that may hand a net over to the cluster tier are laid out with
+// the cluster's capacities (16 CTAs x 4096 agents / variables) plus room for
+// the pending equations, so the hand-over reuses the same device buffers.
+constexpr uint32_t kPromoCapAgents = 16u * 4096u;
+constexpr uint32_t kPromoCapVars = 16u * 4096u;
+constexpr uint32_t kPromoCapQueue = 16384u;
+
+void set_resume(inet_ctx* c, const NetCtl& m) {
+  c->resume.on = true;
+  c->resume.agents = m.agent_bump;
+  c->resume.vars = m.var_bump;
+  c->resume.pending = m.n_residual;
+  c->resume.round_base = m.rounds - 1;
+  c->resume.ints = m.interactions;
+  c->resume.comms = m.communications;
+  c->resume.parked = static_cast<int32_t>(m.parked_total);
+}
+
 Shape base_shape(const inet_ctx* c, uint32_t max_loops) {
   Shape sh{};
   sh.max_rounds = max_loops;
@@ -534,6 +580,9 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   // Try the shared-memory tiers first; a net that overflows sends the whole
   // launch to the next tier (S or M, then G with doubling capacities).
   const bool exact = cfg && cfg->exact_loops;
+  c->promoted = false;
+  c->promo_ms = 0;
+  c->resume.on = false;
   auto attempt_tier = [&](int tier, const Shape& sh0, uint32_t ca, uint32_t cv, uint32_t cq) -> int {
     Shape sh = sh0;
     sh.exact = exact ? 1u : 0u;
@@ -569,9 +618,35 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   // Large single nets: a cluster of G CTAs sharing their shared memory (tier C).
   // Its arenas are fixed by shared memory; a net that outgrows them falls
   // through to the single-CTA tiers.
-  // auto (0): a single net takes a 16-CTA cluster; 1 forces one CTA per net
+  // auto (0): a single net starts on one CTA (tier M, lowest per-round cost);
+  // past 2^19 interactions tier M hands it over — arena, slot table, pending
+  // equations, rounds and totals — and a 16-CTA cluster (tier C) resumes it
+  // from there, which wins once rounds are wide. 1 forces one CTA per net.
   uint32_t want_g = cfg ? cfg->ctas_per_net : 0;
-  if (want_g == 0 && c->n_nets == 1 && !user_caps) want_g = 16;
+  if (want_g == 0 && c->n_nets == 1 && !user_caps) {
+    want_g = 16;
+    if (c->max_in_agents < 32768 && c->max_in_vars < 16384) {
+      Shape sh = base_shape(c, max_loops);
+      sh.res_vars = 14336;
+      sh.res_queue = 5120;
+      sh.ring_a = 8192;
+      sh.ring_v = 8192;
+      sh.promote_ints = c->promote_ints;
+      // capacities that also fit the cluster tier, so the hand-over needs no copy
+      int st = attempt_tier(kTierM, sh, kPromoCapAgents, kPromoCapVars, kPromoCapQueue);
+      if (st == INET_OK && !any_oom() && c->ctl[0].err != inetdev::kPromote) {
+        done = true;
+      } else if (st == INET_OK && c->ctl[0].err == inetdev::kPromote) {
+        c->promoted = true;  // its time counts towards the reduction
+        c->promo_shape = c->shape;
+        c->promo_cap_def = c->cap_def;
+        c->promo_ms = ms;
+        set_resume(c, c->ctl[0]);
+      } else if (st != INET_OK && st != INET_ERR_UNSUPPORTED) {
+        return st;
+      }
+    }
+  }
   if (!done && want_g >= 2 && c->n_nets <= 64) {
     uint32_t G = 2;  // a power of two (ids are owned round-robin: owner = id & (G - 1))
     while (G * 2 <= std::min<uint32_t>(want_g, 16)) G *= 2;
@@ -585,6 +660,10 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     int st = attempt_tier(kTierC, sh, G * sh.res_agents, G * sh.res_vars, 1);
     if (st == INET_OK && !any_oom()) done = true;
     else if (st != INET_OK && st != INET_ERR_UNSUPPORTED) return st;
+    if (!done) {
+      c->resume.on = false;  // the single-CTA tiers below start over from the input
+      c->promoted = false;
+    }
   }
   if (!done && !user_caps && c->n_nets <= 148 && c->max_in_agents < 32768 && c->max_in_vars < 16384) {
     Shape sh = base_shape(c, max_loops);
@@ -613,7 +692,8 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     ca *= 2;
     cv *= 2;
   }
-  if (device_ms) *device_ms = ms;
+  if (c->promoted && c->tier != kTierC) c->promoted = false;  // the cluster fell through: no prefix
+  if (device_ms) *device_ms = ms + (c->promoted ? c->promo_ms : 0.0f);
   c->stats.assign(c->n_nets, inet_net_stats{});
   int first = INET_OK;
   for (uint32_t i = 0; i < c->n_nets; ++i) {
@@ -699,6 +779,27 @@ int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
   c->count_rules = k.count_rules != 0;
   CUDA_TRY(cudaSetDevice(c->device));
   const uint32_t cap_rounds = (k.collect_stats) ? std::min<uint32_t>(k.max_loops + 1u, 1u << 22) : 0;
+  float pre_ms = 0;
+  if (c->promoted) {
+    // replay the single-CTA prefix up to the promotion threshold, then the cluster run
+    const uint32_t ca = c->cap_agents, cv = c->cap_vars, cq = c->cap_queue, cd = c->cap_def;
+    c->cap_def = c->promo_cap_def;
+    c->resume.on = false;
+    int st = layout(c, kPromoCapAgents, kPromoCapVars, kPromoCapQueue, cap_rounds);
+    if (st) return st;
+    Shape ps = c->promo_shape;
+    ps.max_rounds = k.max_loops;
+    st = launch(c, &k, ps, kTierM, &pre_ms);
+    if (st) return st;
+    NetCtl m;
+    CUDA_TRY(cudaMemcpy(&m, c->d_ctl.p, sizeof(NetCtl), cudaMemcpyDeviceToHost));
+    if (m.err != inetdev::kPromote) return INET_ERR_STATE;
+    set_resume(c, m);
+    c->cap_def = cd;
+    c->cap_agents = ca;
+    c->cap_vars = cv;
+    c->cap_queue = cq;
+  }
   int st = layout(c, c->cap_agents, c->cap_vars, c->cap_queue, cap_rounds);
   if (st) return st;
   Shape sh = c->shape;
@@ -706,7 +807,7 @@ int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
   float ms = 0;
   st = launch(c, &k, sh, c->tier, &ms);
   if (st) return st;
-  if (device_ms) *device_ms = ms;
+  if (device_ms) *device_ms = ms + pre_ms;
   return INET_OK;
 }
 
