@@ -738,14 +738,10 @@ template <uint32_t MF, uint32_t MX, int kTier>
 __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uint32_t nx, uint32_t (&f)[MF],
                                                uint32_t (&g)[MX]) {
   if ((nf | nx) == 0) return true;
-  INET_TR(c, 6);
   const uint32_t tv = nf ? atomicAdd(&c.cur->vtake, nf) : 0u;
   const uint32_t ta = nx ? atomicAdd(&c.cur->atake, nx) : 0u;
   const uint32_t av_v = c.hi_v - c.lo_v, av_a = c.hi_a - c.lo_a;
-#ifdef INET_TRACE
-  if ((tv | ta) == 0xFFFFFFFFu) c.tr[7] = 0;
-  c.tr[7] = clock64();
-#endif
+
   const uint32_t gv = tv < av_v ? min(av_v - tv, nf) : 0u, ga = ta < av_a ? min(av_a - ta, nx) : 0u;
   uint32_t bv = 0, ba = 0;
   if (gv < nf) {
@@ -1585,9 +1581,9 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
             const long long t6 = clock64();
             if (r >= INET_TRACE_R0 && r < INET_TRACE_R0 + 2 && ((threadIdx.x & 31u) == 0 || (c.tr[6] != 0)) &&
                 atomicAdd(&inet_trace_count, 1u) < 1200u)
-              printf("TR r=%u k=%u t=%u q+ag=%lld pair=%lld alloc=%lld wr+free=%lld exch=%lld settle=%lld pre=%lld atoms=%lld\n",
+              printf("TR r=%u k=%u t=%u q+ag=%lld pair=%lld alloc=%lld recs+ex+wr+free=%lld push=%lld settle=%lld recs=%lld exissue=%lld\n",
                      r, rank, threadIdx.x, c.tr[2] - c.tr[0], c.tr[2] - c.tr[1], c.tr[3] - c.tr[2], c.tr[4] - c.tr[3],
-                     c.tr[5] - c.tr[4], t6 - c.tr[5], c.tr[6] - c.tr[2], c.tr[7] - c.tr[6]);
+                     c.tr[5] - c.tr[4], t6 - c.tr[5], c.tr[6] - c.tr[3], c.tr[7] - c.tr[6]);
           }
 #endif
         }
