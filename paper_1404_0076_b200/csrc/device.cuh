@@ -47,6 +47,13 @@
 
 #include "../../include/inet_b200.h"
 
+// Reference loop mode code (deferred equations). The rule-set kernels are
+// compiled with and without it: nets whose merges only ever form active pairs
+// (all Ackermann nets) run the smaller kernel and get the same rounds.
+#ifndef INET_EXACT_CODE
+#define INET_EXACT_CODE 1
+#endif
+
 namespace inetdev {
 
 constexpr uint32_t kVar = INET_VAR_BIT;
@@ -100,7 +107,8 @@ struct RoundCtr {
   uint32_t vtake;
   uint32_t vfree;
   uint32_t dcount;  // merged equations deferred to the next round (reference loop mode)
-  uint32_t pad[3];
+  uint32_t vh;      // a merge left a var-headed equation (kernels without INET_EXACT_CODE)
+  uint32_t pad[2];
 };
 
 // Parameters of the next round, written by the last warp to finish a round
@@ -194,11 +202,14 @@ struct Shape {
   uint32_t threads;               // CTA size
   uint32_t exact;                 // 1: reference loop mode (merged var-headed equations wait a round)
   uint32_t promote_ints;          // tier M: give the net up to the cluster tier past this many interactions
-  uint32_t pad;
+  uint32_t detect_vh;             // stop with kNeedExact at the first var-headed merge (exact requested,
+                                  // kernel without INET_EXACT_CODE)
 };
 
-// Internal status of a single-CTA run that outgrew it (not returned to callers).
+// Internal statuses (never returned to callers): a single-CTA run that outgrew
+// it; a run without reference-loop code that met a var-headed merge.
 constexpr uint32_t kPromote = 0x100u;
+constexpr uint32_t kNeedExact = 0x101u;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -591,18 +602,19 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
       push_active(c, l, r);
       return;
     }
+#if INET_EXACT_CODE
     if (c.dout) {
       // reference loop mode: the merged equation communicates next round, as
-      // it would in the reference's next communication_phase (engine.py:137-166)
-      const uint32_t p = atomicAdd(&c.cur->dcount, 1u);
-      if (p >= c.cap_def) {
-        fail(c, INET_ERR_ARENA, 3);
-        return;
-      }
-      c.dout[p] = make_uint2(l, r);
+      // it would in the reference's next communication_phase (engine.py:137-166).
+      // (Kept minimal — settle is inlined at every equation of every rule; a
+      // full buffer is reported when the round closes.)
+      c.dout[min(atomicAdd(&c.cur->dcount, 1u), c.cap_def - 1)] = make_uint2(l, r);
       c.parked += 1;  // live until linked
       return;
     }
+#else
+    c.cur->vh = 1u;  // noted; a run that wants reference loops restarts with the full kernel
+#endif
     uint32_t key;
     key_of(l, r, key, val);
     x = key & ~kVar;
@@ -1101,7 +1113,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     c.dout = sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
     c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + (r & 1u) * qstride)
                        : static_cast<void*>(static_cast<uint2*>(q0) + (r & 1u) * qstride);
-    if (h.nd) {
+    if (INET_EXACT_CODE && h.nd) {
       // equations merged last round that are still var-headed: this round's
       // communication links them (reference loop mode)
       const uint2* din = d.deferred + ((r - 1) & 1u) * d.cap_def;
@@ -1202,10 +1214,16 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       nh.hi_a = h.hi_a + wa;
       nh.lo_v = h.lo_v + min(k.vtake, h.hi_v - h.lo_v);
       nh.hi_v = h.hi_v + wv;
+#if INET_EXACT_CODE
+      if (k.dcount > d.cap_def && atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_ARENA)) == 0u) {
+        ctl->err_a = 3;
+        k.qcount |= kErrBit;
+      }
+#endif
       const bool round_failed = (k.qcount & kErrBit) != 0;
       k.qcount &= ~kErrBit;
       nh.n = k.qcount;
-      nh.nd = k.dcount;
+      nh.nd = INET_EXACT_CODE ? k.dcount : 0u;
       nh.stop = 0;
       const int32_t parked = ctl->parked_total + k.parked;
       ctl->parked_total = parked;
@@ -1223,14 +1241,17 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       ctl->rounds = r + 1;
       if (round_failed) {
         nh.stop = 1;
-      } else if (k.qcount == 0 && k.dcount == 0) {
+      } else if (k.qcount == 0 && (!INET_EXACT_CODE || k.dcount == 0)) {
         // the trailing no-op loop the reference records (engine.py:222-223)
         nh.stop = 1;
         if (d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked), 0);
+      } else if (!INET_EXACT_CODE && sh.detect_vh && k.vh) {
+        nh.stop = 1;  // the host reruns the net with reference-loop code
+        atomicCAS(&ctl->err_code, 0u, kNeedExact);
       } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
         nh.stop = 1;
         atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_LOOP_CAP));
-      } else if (sh.promote_ints && ctl->tot_i >= sh.promote_ints) {
+      } else if (kTier == kTierM && sh.promote_ints && ctl->tot_i >= sh.promote_ints) {
         nh.stop = 1;  // a large net: the host reruns it on a cluster
         atomicCAS(&ctl->err_code, 0u, kPromote);
       }
@@ -1531,7 +1552,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
         }
       }
     }
-    if (r > 1 && sh.exact) {
+    if (INET_EXACT_CODE && r > 1 && sh.exact) {
       // this CTA's equations merged last round that are still var-headed
       const uint32_t nd = ctr3[(r - 1) % 3].dcount;
       const uint2* din = d.deferred + (((r - 1) & 1u) * G + rank) * c.cap_def;
@@ -1602,11 +1623,16 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     }
     // every CTA pushes its round counters into every CTA's inbox
     __syncthreads();
+    if (threadIdx.x == 0 && cur->dcount > c.cap_def) {  // deferred buffer overflowed
+      if (atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_ARENA)) == 0u) ctl->err_a = 3;
+      atomicOr(&cur->qcount, kErrBit);
+    }
+    __syncthreads();
     if (threadIdx.x < G) {
       const uint32_t k = threadIdx.x;
       uint4* dst = &inbox[(r % 3) * 32 + 2 * rank];
       dsmem_st4(dst, k, make_uint4(cur->qcount, cur->ints, cur->comms, static_cast<uint32_t>(cur->parked)));
-      dsmem_st4(dst + 1, k, make_uint4(c.outc[k], c.outc[16 + k], cur->dcount, 0u));
+      dsmem_st4(dst + 1, k, make_uint4(c.outc[k], c.outc[16 + k], cur->dcount, cur->vh));
     }
     CT_MARK(2);
     cluster_barrier();
@@ -1619,6 +1645,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     uint32_t total;  // pairs queued cluster-wide
     warp_excl_scan(w.x, lane, total);
     const bool deferred_any = __any_sync(0xFFFFFFFFu, lane < G && inbox[(r % 3) * 32 + 2 * lane + 1].z != 0);
+    const bool vh_any = sh.detect_vh && __any_sync(0xFFFFFFFFu, lane < G && inbox[(r % 3) * 32 + 2 * lane + 1].w != 0);
     // pairs producer `lane` dealt to this CTA: its p-th went to CTA (p + lane) mod G
     uint32_t mine;
     {
@@ -1662,6 +1689,9 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     N = mine;
     if (err_any) {
       stop = true;
+    } else if (vh_any) {
+      stop = true;  // the host reruns the net with reference-loop code
+      stop_err = kNeedExact;
     } else if (total == 0 && !deferred_any) {
       stop = true;  // the trailing no-op loop the reference records (engine.py:222-223)
     } else if (rb + r + 1 > sh.max_rounds) {  // engine.py:205-207

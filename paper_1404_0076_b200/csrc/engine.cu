@@ -207,6 +207,7 @@ struct inet_ctx {
   std::string jit_log;
   std::map<std::tuple<int, uint32_t, int>, std::pair<cudaLibrary_t, cudaKernel_t>> jit_kernels;
   int jit_style = -1;  // -1: per tier (measured defaults); env INET_B200_JITSTYLE overrides
+  bool exact_code = true;  // rule-set kernel variant with reference-loop (deferred equation) code
 };
 
 inline uint32_t hist_stride(const inet_ctx* c) { return std::max(c->n_rules, 128u); }
@@ -447,10 +448,10 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
   // code style per tier: straight-line cases where the rewrite is issue-bound
   // (S, M, G); a uniform memory phase where remote latency dominates (C)
   const int style = c->jit_style >= 0 ? c->jit_style : (tier == kTierC ? 1 : 0);
-  const auto key = std::make_tuple(tier, threads, style);
+  const auto key = std::make_tuple(tier, threads, style + (c->exact_code ? 16 : 0));
   auto it = c->jit_kernels.find(key);
   if (it != c->jit_kernels.end()) return reinterpret_cast<const void*>(it->second.second);
-  const std::string src = inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style);
+  const std::string src = inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style, c->exact_code);
   std::vector<char> cubin;
   if (inetjit::compile_cubin(src, cubin, c->jit_log) != 0) {
     std::fprintf(stderr, "inet_b200: rule-set JIT unavailable, using the prebuilt kernels: %s\n", c->jit_log.c_str());
@@ -576,19 +577,28 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     return INET_OK;
   };
   const bool user_caps = cfg && (cfg->cap_agents || cfg->cap_vars);
-  bool done = false;
-  // Try the shared-memory tiers first; a net that overflows sends the whole
-  // launch to the next tier (S or M, then G with doubling capacities).
+  // Reference loop mode: the rule-set kernel is first run without the
+  // deferred-equation code (smaller and faster); it stops at the first merge
+  // that leaves a var-headed equation (kNeedExact), and only then is the net
+  // rerun with the full kernel. Nets whose merges only form active pairs (all
+  // Ackermann nets) never need it, and their rounds are the reference's loops.
   const bool exact = cfg && cfg->exact_loops;
+  bool with_defer = exact && !c->jit_mode;  // the prebuilt kernels always carry the code
+  for (int pass = 0; pass < 2; ++pass) {
+  c->exact_code = with_defer || !c->jit_mode;
+  bool done = false;
   c->promoted = false;
   c->promo_ms = 0;
   c->resume.on = false;
+  // Try the shared-memory tiers first; a net that overflows sends the whole
+  // launch to the next tier (S or M, then G with doubling capacities).
   auto attempt_tier = [&](int tier, const Shape& sh0, uint32_t ca, uint32_t cv, uint32_t cq) -> int {
     Shape sh = sh0;
-    sh.exact = exact ? 1u : 0u;
+    sh.exact = exact && c->exact_code ? 1u : 0u;
+    sh.detect_vh = exact && !c->exact_code ? 1u : 0u;
     // deferred equations per round: the round's queue size is a safe bound in
     // practice; an overflow reports ARENA and the next attempt grows it
-    c->cap_def = exact ? (tier == kTierC ? c->cluster_g * 1024u : std::max<uint32_t>(256u, tier == kTierG ? cq : sh.res_queue))
+    c->cap_def = sh.exact ? (tier == kTierC ? c->cluster_g * 1024u : std::max<uint32_t>(256u, tier == kTierG ? cq : sh.res_queue))
                        : 0u;
     int st = layout(c, ca, cv, cq, cap_rounds);
     if (st) return st;
@@ -691,6 +701,12 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     if (uint64_t(ca) * 2 >= INET_VAR_BIT || uint64_t(cv) * 2 >= INET_VAR_BIT) break;
     ca *= 2;
     cv *= 2;
+  }
+  if (!exact || c->exact_code) break;
+  bool need = false;
+  for (uint32_t i = 0; i < c->n_nets; ++i) need |= c->ctl[i].err == inetdev::kNeedExact;
+  if (!need) break;
+  with_defer = true;
   }
   if (c->promoted && c->tier != kTierC) c->promoted = false;  // the cluster fell through: no prefix
   if (device_ms) *device_ms = ms + (c->promoted ? c->promo_ms : 0.0f);
@@ -826,7 +842,10 @@ int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t th
   std::string msg;
   int style = tier == kTierC ? 1 : 0;
   if (const char* e = std::getenv("INET_B200_JITSTYLE")) style = std::atoi(e);
-  const int rc = inetjit::compile_cubin(inetjit::kernel_source(blob, n_words, tier, threads, style), cubin, msg);
+  bool exact_code = true;
+  if (const char* e = std::getenv("INET_B200_EXACTCODE")) exact_code = std::atoi(e) != 0;
+  const int rc =
+      inetjit::compile_cubin(inetjit::kernel_source(blob, n_words, tier, threads, style, exact_code), cubin, msg);
   if (log && log_len) {
     std::strncpy(log, msg.c_str(), log_len - 1);
     log[log_len - 1] = 0;

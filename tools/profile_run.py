@@ -14,6 +14,7 @@ ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--jit", type=int, default=1)
 ap.add_argument("--g", type=int, default=0, help="CTAs per net (tier C cluster)")
+ap.add_argument("--exact", type=int, default=1, help="reference loop mode")
 a = ap.parse_args()
 spec = {"a38": ("ackermann", (3, 8), 1), "a310": ("ackermann", (3, 10), 1), "fib18": ("fibonacci", (18,), 1),
         "batch": ("ackermann", (3, 6), a.nets)}[a.workload]
@@ -23,7 +24,7 @@ ctx = _native.Context(0)
 ctx.set_jit(bool(a.jit))
 ctx.load_rules(prep.blob)
 ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
-k = engine.native_cfg(EngineConfig(collect_stats=False, threads=a.threads, ctas_per_net=a.g))
+k = engine.native_cfg(EngineConfig(collect_stats=False, threads=a.threads, ctas_per_net=a.g, exact_loops=bool(a.exact)))
 for _ in range(a.repeat):
     code, ms = ctx.reduce(k)
     st = ctx.stats(0)
