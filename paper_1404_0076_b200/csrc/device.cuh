@@ -123,7 +123,7 @@ struct Header {
 
 // Shared-memory control block of the net a CTA is reducing.
 struct Ctl {
-  RoundCtr ctr;
+  RoundCtr ctr3[3];  // tiers S/M/G: round r counts into set r % 3 (cleared two rounds ahead)
   Header hdr;
   uint32_t done_warps;
   uint32_t agent_bump;
@@ -1071,53 +1071,56 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += blockDim.x) w[i] = 0;
   }
   __syncthreads();
+  // Round state, kept identically by every thread: each thread closes every
+  // round itself from the round's counters, so a round ends with one barrier
+  // and no serial bookkeeping warp.
+  bool stop = false;
+  uint32_t stop_err = 0;
   if (threadIdx.x == 0) {
     ctl->agent_bump = d.n_in_agents;
     ctl->var_bump = d.n_in_vars;
-    ctl->hdr.n = d.n_in_eqs;
-    ctl->t_prev = globaltimer();
-    ctl->rounds = 1;
-    if (!fits) {
-      ctl->err_code = INET_ERR_ARENA;
-      ctl->hdr.stop = 1;
-    } else if (d.n_in_eqs == 0) {  // one no-op loop (engine.py:222-223)
-      ctl->hdr.stop = 1;
-      if (d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
-    } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207)
-      ctl->err_code = INET_ERR_LOOP_CAP;
-      ctl->hdr.stop = 1;
-    }
+  }
+  if (!fits) {
+    stop = true;
+    stop_err = INET_ERR_ARENA;
+  } else if (d.n_in_eqs == 0) {  // one no-op loop (engine.py:222-223)
+    stop = true;
+    if (threadIdx.x == 0 && d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
+  } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207)
+    stop = true;
+    stop_err = INET_ERR_LOOP_CAP;
   }
   __syncthreads();
   c.failed = false;
-  c.cur = &ctl->ctr;
   c.env = smem + plan.env_off + threadIdx.x;
   if constexpr (T::kEnvSmem) c.env[(kEnvSize - 1) * blockDim.x] = kNone;  // (disabled tier option)
 #ifdef INET_TIMING
   for (int i = 0; i < 8; ++i) c.tm[i] = 0;
   c.tlast = clock64();
 #endif
-  const uint32_t n_warps = (blockDim.x + 31u) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
   c.cap_def = d.cap_def;
-  for (uint32_t r = 1;; ++r) {
-    const Header h = ctl->hdr;
-    if (h.stop) break;
-    const uint32_t n = h.n;
-    c.lo_a = h.lo_a;
-    c.hi_a = h.hi_a;
-    c.lo_v = h.lo_v;
-    c.hi_v = h.hi_v;
+  uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, nd = 0, rounds = 1;
+  int32_t parked_tot = 0;
+  unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
+  for (uint32_t r = 1; !stop; ++r) {
+    RoundCtr* cur = &ctl->ctr3[r % 3];
+    c.cur = cur;
+    c.lo_a = lo_a;
+    c.hi_a = hi_a;
+    c.lo_v = lo_v;
+    c.hi_v = hi_v;
     c.ints = c.comms = 0;
     c.parked = 0;
+    if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(&ctl->ctr3[(r + 1) % 3])[threadIdx.x] = 0;
     c.dout = sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
     c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + (r & 1u) * qstride)
                        : static_cast<void*>(static_cast<uint2*>(q0) + (r & 1u) * qstride);
-    if (INET_EXACT_CODE && h.nd) {
+    if (INET_EXACT_CODE && nd) {
       // equations merged last round that are still var-headed: this round's
       // communication links them (reference loop mode)
       const uint2* din = d.deferred + ((r - 1) & 1u) * d.cap_def;
-      for (uint32_t i = threadIdx.x; i < h.nd && !c.failed; i += blockDim.x) {
+      for (uint32_t i = threadIdx.x; i < nd && !c.failed; i += blockDim.x) {
         const uint2 eq = din[i];
         c.parked -= 1;
         link(c, eq.x, eq.y);
@@ -1179,89 +1182,79 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       }
     }
     INET_TMARK(c, 5);
-    const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
-    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
-    const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
-    __syncwarp();
-    uint32_t last = 0;
-    if (lane == 0) {
-      if (wi) atomicAdd(&c.cur->ints, wi);
-      if (wc) atomicAdd(&c.cur->comms, wc);
-      if (wp) atomicAdd(&c.cur->parked, wp);
-#ifndef INET_NO_FENCE
-      __threadfence_block();
-#endif
-      last = atomicAdd(&ctl->done_warps, 1u) == n_warps - 1;
+    {
+      const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
+      const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
+      const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
+      if (lane == 0) {
+        if (wi) atomicAdd(&cur->ints, wi);
+        if (wc) atomicAdd(&cur->comms, wc);
+        if (wp) atomicAdd(&cur->parked, wp);
+      }
     }
-    if (last) {
-      // every other warp has finished round r: close it and open round r+1
-#ifndef INET_NO_FENCE
-      __threadfence_block();
-#endif
-      RoundCtr k;
-      {
-        const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(&ctl->ctr);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(&k);
-#pragma unroll
-        for (int i = 0; i < static_cast<int>(sizeof(RoundCtr) / 4); ++i) dst[i] = src[i];
-      }
-      Header nh;
-      nh.pad = 0;
-      // frees of round r were kept while they fit the ring (against its old window)
-      const uint32_t wa = min(k.afree, sh.ring_a - (h.hi_a - h.lo_a));
-      const uint32_t wv = min(k.vfree, sh.ring_v - (h.hi_v - h.lo_v));
-      nh.lo_a = h.lo_a + min(k.atake, h.hi_a - h.lo_a);
-      nh.hi_a = h.hi_a + wa;
-      nh.lo_v = h.lo_v + min(k.vtake, h.hi_v - h.lo_v);
-      nh.hi_v = h.hi_v + wv;
+    INET_TMARK(c, 6);
+    __syncthreads();
+    INET_TMARK(c, 7);
+    // ---- close round r (every thread, same values)
+    const RoundCtr k = *cur;
+    bool round_failed = (k.qcount & kErrBit) != 0;
+    const uint32_t q = k.qcount & ~kErrBit;
 #if INET_EXACT_CODE
-      if (k.dcount > d.cap_def && atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_ARENA)) == 0u) {
-        ctl->err_a = 3;
-        k.qcount |= kErrBit;
-      }
+    if (k.dcount > d.cap_def) {
+      round_failed = true;
+      if (threadIdx.x == 0 && atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_ARENA)) == 0u) ctl->err_a = 3;
+    }
 #endif
-      const bool round_failed = (k.qcount & kErrBit) != 0;
-      k.qcount &= ~kErrBit;
-      nh.n = k.qcount;
-      nh.nd = INET_EXACT_CODE ? k.dcount : 0u;
-      nh.stop = 0;
-      const int32_t parked = ctl->parked_total + k.parked;
-      ctl->parked_total = parked;
-      ctl->tot_i += k.ints;
-      ctl->tot_c += k.comms;
+    // frees of round r were kept while they fit the ring (against its old window)
+    const uint32_t wa = min(k.afree, sh.ring_a - (hi_a - lo_a));
+    const uint32_t wv = min(k.vfree, sh.ring_v - (hi_v - lo_v));
+    lo_a += min(k.atake, hi_a - lo_a);
+    hi_a += wa;
+    lo_v += min(k.vtake, hi_v - lo_v);
+    hi_v += wv;
+    parked_tot += k.parked;
+    tot_i += k.ints;
+    tot_c += k.comms;
+    if (threadIdx.x == 0 && d.stats) {
 #ifdef INET_NO_TIMER
       const unsigned long long now = 0;
 #else
       const unsigned long long now = globaltimer();
 #endif
-      if (d.stats && r - 1 < d.cap_rounds)
-        d.stats[r - 1] = make_uint4(k.ints, k.comms, k.qcount + static_cast<uint32_t>(parked),
-                                    static_cast<uint32_t>(now - ctl->t_prev));
-      ctl->t_prev = now;
-      ctl->rounds = r + 1;
-      if (round_failed) {
-        nh.stop = 1;
-      } else if (k.qcount == 0 && (!INET_EXACT_CODE || k.dcount == 0)) {
-        // the trailing no-op loop the reference records (engine.py:222-223)
-        nh.stop = 1;
-        if (d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked), 0);
-      } else if (!INET_EXACT_CODE && sh.detect_vh && k.vh) {
-        nh.stop = 1;  // the host reruns the net with reference-loop code
-        atomicCAS(&ctl->err_code, 0u, kNeedExact);
-      } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
-        nh.stop = 1;
-        atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_LOOP_CAP));
-      } else if (kTier == kTierM && sh.promote_ints && ctl->tot_i >= sh.promote_ints) {
-        nh.stop = 1;  // a large net: the host reruns it on a cluster
-        atomicCAS(&ctl->err_code, 0u, kPromote);
-      }
-      ctl->ctr = RoundCtr{};
-      ctl->hdr = nh;
-      ctl->done_warps = 0;
+      if (r - 1 < d.cap_rounds)
+        d.stats[r - 1] = make_uint4(k.ints, k.comms, q + static_cast<uint32_t>(parked_tot),
+                                    static_cast<uint32_t>(now - t_prev));
+      t_prev = now;
     }
-    INET_TMARK(c, 6);
-    __syncthreads();
-    INET_TMARK(c, 7);
+    rounds = r + 1;
+    n = q;
+    nd = INET_EXACT_CODE ? k.dcount : 0u;
+    if (round_failed) {
+      stop = true;
+    } else if (q == 0 && nd == 0) {
+      // the trailing no-op loop the reference records (engine.py:222-223)
+      stop = true;
+      if (threadIdx.x == 0 && d.stats && r < d.cap_rounds)
+        d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
+    } else if (!INET_EXACT_CODE && sh.detect_vh && k.vh) {
+      stop = true;  // the host reruns the net with reference-loop code
+      stop_err = kNeedExact;
+    } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
+      stop = true;
+      stop_err = INET_ERR_LOOP_CAP;
+    } else if (kTier == kTierM && sh.promote_ints && tot_i >= sh.promote_ints) {
+      stop = true;  // a large net: the host hands it over to a cluster
+      stop_err = kPromote;
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (stop_err) atomicCAS(&ctl->err_code, 0u, stop_err);
+    ctl->rounds = rounds;
+    ctl->tot_i = tot_i;
+    ctl->tot_c = tot_c;
+    ctl->parked_total = parked_tot;
+    ctl->hdr.n = n;
+    ctl->hdr.nd = nd;
   }
 #ifdef INET_TIMING
   if (d.rule_hist)
