@@ -617,6 +617,15 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
       sh.res_queue = cap / 2;
       sh.ring_a = cap;
       sh.ring_v = cap;
+      if (const char* e = std::getenv("INET_B200_SCAP")) {  // development: agents,vars,queue,ring
+        unsigned a = 0, v = 0, q = 0, rg = 0;
+        if (std::sscanf(e, "%u,%u,%u,%u", &a, &v, &q, &rg) == 4 && cap == 1024u) {
+          sh.res_agents = a;
+          sh.res_vars = v;
+          sh.res_queue = q;
+          sh.ring_a = sh.ring_v = rg;
+        }
+      }
       int st = attempt_tier(kTierS, sh, sh.res_agents, sh.res_vars, 1);
       if (st == INET_OK && !any_oom()) {
         done = true;
