@@ -1477,7 +1477,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   int32_t parked_tot = d.base_parked;
   const uint32_t rb = d.round_base;  // rounds done before this launch (resume)
   uint32_t N = d.n_in_eqs, excl = 0, rounds = 1, stop_err = 0;
-  bool stop = false;
+  bool stop = false, mail_any = false;
   const bool writer = rank == 0 && threadIdx.x == 0;
   if (!fits) {
     stop = true;
@@ -1509,7 +1509,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     }
     // mail of round r-1: move the ids other CTAs freed for this one into its rings
     // (the top warps do it; pairs go to the low threads first)
-    if (r > 1) {
+    if (r > 1 && mail_any) {
       const uint32_t ma = lane < G ? min(inbox[((r - 1) % 3) * 32 + 2 * lane + 1].x, kMbox) : 0u;
       const uint32_t mv = lane < G ? min(inbox[((r - 1) % 3) * 32 + 2 * lane + 1].y, kMbox) : 0u;
       uint32_t ta, tv;
@@ -1616,11 +1616,13 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     }
     // every CTA pushes its round counters into every CTA's inbox
     __syncthreads();
+#if INET_EXACT_CODE
     if (threadIdx.x == 0 && cur->dcount > c.cap_def) {  // deferred buffer overflowed
       if (atomicCAS(&ctl->err_code, 0u, static_cast<uint32_t>(INET_ERR_ARENA)) == 0u) ctl->err_a = 3;
       atomicOr(&cur->qcount, kErrBit);
     }
     __syncthreads();
+#endif
     if (threadIdx.x < G) {
       const uint32_t k = threadIdx.x;
       uint4* dst = &inbox[(r % 3) * 32 + 2 * rank];
@@ -1637,8 +1639,10 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     w.x &= ~kErrBit;
     uint32_t total;  // pairs queued cluster-wide
     warp_excl_scan(w.x, lane, total);
-    const bool deferred_any = __any_sync(0xFFFFFFFFu, lane < G && inbox[(r % 3) * 32 + 2 * lane + 1].z != 0);
-    const bool vh_any = sh.detect_vh && __any_sync(0xFFFFFFFFu, lane < G && inbox[(r % 3) * 32 + 2 * lane + 1].w != 0);
+    const uint4 w2 = lane < G ? inbox[(r % 3) * 32 + 2 * lane + 1] : make_uint4(0, 0, 0, 0);
+    const bool deferred_any = __any_sync(0xFFFFFFFFu, w2.z != 0);
+    mail_any = __any_sync(0xFFFFFFFFu, (w2.x | w2.y) != 0);  // mail for this CTA, moved next round
+    const bool vh_any = sh.detect_vh && __any_sync(0xFFFFFFFFu, w2.w != 0);
     // pairs producer `lane` dealt to this CTA: its p-th went to CTA (p + lane) mod G
     uint32_t mine;
     {
