@@ -415,11 +415,11 @@ __device__ __forceinline__ uint32_t dsmem_exch(const void* p, uint32_t rank, uin
 // Tier S keeps agents as 8 bytes {label, p0 | p1, p2} with 16-bit refs
 // (bit 15 = variable, 0xFFFF = none; its arenas hold < 32768 ids), which
 // fits more nets per SM.
-__device__ __forceinline__ uint32_t ref16(uint32_t r) {
-  return r == kNone ? 0xFFFFu : ((r & kVar) ? (0x8000u | (r & 0x7FFFu)) : (r & 0x7FFFu));
-}
+// Branch-free: kNone maps to 0xFFFF and back because variable 0x7FFF never
+// exists in these arenas (< 32768 ids, the top one unused).
+__device__ __forceinline__ uint32_t ref16(uint32_t r) { return ((r >> 16) & 0x8000u) | (r & 0x7FFFu); }
 __device__ __forceinline__ uint32_t ref32(uint32_t h) {
-  return h == 0xFFFFu ? kNone : ((h & 0x8000u) ? (kVar | (h & 0x7FFFu)) : h);
+  return ((h & 0x8000u) << 16) | (h & 0x7FFFu) | (((h + 1u) >> 16) * 0x7FFF8000u);
 }
 __device__ __forceinline__ uint2 pack_agent(const uint4& v) {
   return make_uint2(v.x | (ref16(v.y) << 16), ref16(v.z) | (ref16(v.w) << 16));
