@@ -1512,10 +1512,15 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     if (r > 1 && mail_any) {
       const uint32_t ma = lane < G ? min(inbox[((r - 1) % 3) * 32 + 2 * lane + 1].x, kMbox) : 0u;
       const uint32_t mv = lane < G ? min(inbox[((r - 1) % 3) * 32 + 2 * lane + 1].y, kMbox) : 0u;
-      uint32_t ta, tv;
-      const uint32_t xa = warp_excl_scan(ma, lane, ta), xv = warp_excl_scan(mv, lane, tv);
+      const uint32_t ta = __reduce_add_sync(0xFFFFFFFFu, ma), tv = __reduce_add_sync(0xFFFFFFFFu, mv);
       const uint32_t* pm = mbox + ((r - 1) & 1u) * 2 * 16 * kMbox;
       const uint32_t nw = kBlock / 32;
+      // only the warps that copy need the per-source offsets
+      uint32_t xa = 0, xv = 0, dummy;
+      if ((nw - 1 - warp) * 32 < ta + tv) {
+        xa = warp_excl_scan(ma, lane, dummy);
+        xv = warp_excl_scan(mv, lane, dummy);
+      }
       for (uint32_t eb = (nw - 1 - warp) * 32; eb < ta + tv; eb += kBlock) {
         const uint32_t e = eb + lane;
         const bool is_a = e < ta;
@@ -1637,8 +1642,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     if (lane < G) w = inbox[(r % 3) * 32 + 2 * lane];
     const bool err_any = __any_sync(0xFFFFFFFFu, (w.x & kErrBit) != 0);
     w.x &= ~kErrBit;
-    uint32_t total;  // pairs queued cluster-wide
-    warp_excl_scan(w.x, lane, total);
+    const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, w.x);  // pairs queued cluster-wide
     const uint4 w2 = lane < G ? inbox[(r % 3) * 32 + 2 * lane + 1] : make_uint4(0, 0, 0, 0);
     const bool deferred_any = __any_sync(0xFFFFFFFFu, w2.z != 0);
     mail_any = __any_sync(0xFFFFFFFFu, (w2.x | w2.y) != 0);  // mail for this CTA, moved next round
