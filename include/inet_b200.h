@@ -122,6 +122,9 @@ typedef struct inet_net_stats {
 int inet_ctx_create(int device, inet_ctx** out);
 void inet_ctx_destroy(inet_ctx* ctx);
 const char* inet_strerror(int status);
+/* sizeof(inet_cfg) and sizeof(inet_net_stats) as compiled into the library,
+ * so a binding can check its struct layouts (no device needed). */
+void inet_abi_sizes(size_t* cfg_bytes, size_t* stats_bytes);
 /* Device properties for reporting: SM count and clock (kHz). */
 int inet_device_info(inet_ctx* ctx, int* sm_count, int* clock_khz, char* name, size_t name_len);
 

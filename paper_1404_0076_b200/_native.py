@@ -24,6 +24,7 @@ EXPORTS = (
     "inet_ctx_create",
     "inet_ctx_destroy",
     "inet_strerror",
+    "inet_abi_sizes",
     "inet_device_info",
     "inet_rules_load",
     "inet_set_jit",
@@ -95,6 +96,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             "inet_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
             "inet_ctx_destroy": (None, [C.c_void_p]),
             "inet_strerror": (C.c_char_p, [C.c_int]),
+            "inet_abi_sizes": (None, [C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
             "inet_device_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
             "inet_rules_load": (C.c_int, [C.c_void_p, _u32p, C.c_size_t]),
             "inet_set_jit": (C.c_int, [C.c_void_p, C.c_int]),
@@ -121,6 +123,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        cfg_b, st_b = C.c_size_t(), C.c_size_t()
+        lib.inet_abi_sizes(C.byref(cfg_b), C.byref(st_b))
+        if cfg_b.value != C.sizeof(Cfg) or st_b.value != C.sizeof(NetStats):
+            raise DeviceError(-1, f"ABI mismatch: inet_cfg {cfg_b.value} vs {C.sizeof(Cfg)} bytes, "
+                                  f"inet_net_stats {st_b.value} vs {C.sizeof(NetStats)} bytes")
         _lib = lib
         return lib
 

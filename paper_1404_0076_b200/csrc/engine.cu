@@ -248,6 +248,11 @@ const char* inet_strerror(int status) {
   }
 }
 
+void inet_abi_sizes(size_t* cfg_bytes, size_t* stats_bytes) {
+  if (cfg_bytes) *cfg_bytes = sizeof(inet_cfg);
+  if (stats_bytes) *stats_bytes = sizeof(inet_net_stats);
+}
+
 int inet_ctx_create(int device, inet_ctx** out) {
   if (!out) return INET_ERR_ARG;
   *out = nullptr;

@@ -254,3 +254,14 @@ def test_context_without_device_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(errors.DeviceError):
         _native.Context(0)
+
+
+def test_abi_struct_sizes_match_the_library():
+    """The ctypes mirrors of inet_cfg / inet_net_stats have the library's layout (no GPU needed)."""
+    import ctypes as C
+    from paper_1404_0076_b200 import _native
+    lib = _native.load_library()
+    cfg_b, st_b = C.c_size_t(), C.c_size_t()
+    lib.inet_abi_sizes(C.byref(cfg_b), C.byref(st_b))
+    assert cfg_b.value == C.sizeof(_native.Cfg)
+    assert st_b.value == C.sizeof(_native.NetStats)
