@@ -88,7 +88,9 @@ typedef struct inet_cfg {
   uint32_t max_loops;     /* LoopCapExceeded when round > max_loops */
   uint32_t collect_stats; /* record per-round rows (LoopStats) */
   uint32_t threads;       /* CTA size per net; 0 = auto */
-  uint32_t ctas_per_net;  /* 1 = one CTA per net; 0 = auto (large single nets use a cluster) */
+  uint32_t ctas_per_net;  /* 0 = auto: a single net starts on one CTA, moves to a 16-CTA cluster past
+                             2^19 interactions, and to the whole GPU if it outgrows the cluster;
+                             1 = one CTA per net; 2..16 = that cluster size; > 16 = the whole GPU */
   uint32_t cap_agents;    /* initial per-net agent arena; 0 = auto (grows on overflow) */
   uint32_t cap_vars;      /* initial per-net variable table; 0 = auto (grows on overflow) */
   uint32_t max_retries;   /* arena doublings before INET_ERR_ARENA; 0 = default */

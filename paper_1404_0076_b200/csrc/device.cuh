@@ -66,7 +66,7 @@ constexpr int kRuleWords = 16;
 constexpr int kFastEq = 4;  // rhs equations linked with overlapped exchanges
 constexpr uint32_t kMbox = 64;  // tier C: ids one CTA can mail to one owner per round (then direct frees)
 
-enum : int { kTierS = 0, kTierM = 1, kTierG = 2, kTierC = 3 };
+enum : int { kTierS = 0, kTierM = 1, kTierG = 2, kTierC = 3, kTierX = 4 };
 
 template <int kTier>
 struct Traits {
@@ -92,6 +92,10 @@ struct Traits<kTierG> {
 // global memory (L2-resident), rings and round counters per CTA.
 template <>
 struct Traits<kTierC> : Traits<kTierG> {};
+// Tier X: one net on the whole GPU (one CTA per SM slot, cooperative launch);
+// everything, counters included, in global memory (L2-resident).
+template <>
+struct Traits<kTierX> : Traits<kTierG> {};
 
 // Counters of the running round, bumped by every thread while it works.
 // (Tier C reads {qcount, ints, comms, parked} of every CTA with one 16-byte
@@ -164,6 +168,14 @@ __device__ __forceinline__ uint32_t clock_mhz(long long c0, unsigned long long g
   return dg ? static_cast<uint32_t>(static_cast<unsigned long long>(dc) * 1000ull / dg) : 0u;
 }
 
+// Tier X: the control block of a net reduced by the whole grid.
+struct GridState {
+  Ctl ctl;
+  RoundCtr ctr3[3];
+  uint32_t bar_count, bar_gen;
+  uint32_t blk_res[1];  // per-block residual counts follow (gridDim.x words)
+};
+
 // Per-net device view of its private global arrays.
 struct NetDesc {
   uint4* agents;       // cap_agents (tiers M/G arena; tier S result copy)
@@ -188,6 +200,10 @@ struct NetDesc {
   unsigned long long base_ints, base_comms;
   int32_t base_parked;
   uint32_t pad3;
+  // tier X: global free rings and the net's global control block
+  uint32_t* g_aring;
+  uint32_t* g_vring;
+  struct GridState* gs;
 };
 
 // Launch-wide shape: ring sizes and the shared-memory capacities.
@@ -489,6 +505,17 @@ __device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, Claim&
   return true;
 }
 
+// atomicAdd(p, 1) shared by the converged lanes of the warp: one atomic per
+// warp (tier X counters are global and hot).
+__device__ __forceinline__ uint32_t agg_add(uint32_t* p) {
+  const uint32_t m = __activemask();
+  const uint32_t lane = threadIdx.x & 31u, leader = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(p, static_cast<uint32_t>(__popc(m)));
+  base = __shfl_sync(m, base, leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
 template <int kTier>
 __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
   if constexpr (kTier == kTierC) {
@@ -496,7 +523,7 @@ __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
                static_cast<uint32_t*>(nullptr));
     return;
   }
-  const uint32_t f = atomicAdd(&c.cur->afree, 1u);
+  const uint32_t f = kTier == kTierX ? agg_add(&c.cur->afree) : atomicAdd(&c.cur->afree, 1u);
   const uint32_t pos = c.hi_a + f;
   if (pos - c.lo_a <= c.amask) c.aring[pos & c.amask] = a;  // else dropped
 }
@@ -508,7 +535,7 @@ __device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
                c.mbox_v, c.vslot);
     return;
   }
-  const uint32_t f = atomicAdd(&c.cur->vfree, 1u);
+  const uint32_t f = kTier == kTierX ? agg_add(&c.cur->vfree) : atomicAdd(&c.cur->vfree, 1u);
   const uint32_t pos = c.hi_v + f;
   if (pos - c.lo_v <= c.vmask) c.vring[pos & c.vmask] = x;
 }
@@ -522,7 +549,7 @@ __device__ __forceinline__ void dsmem_st2(const void* p, uint32_t rank, uint2 v)
 // consumer's shared memory, so next round every CTA reads its pairs locally.
 template <int kTier>
 __device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_t r) {
-  const uint32_t p = atomicAdd(&c.cur->qcount, 1u);
+  const uint32_t p = kTier == kTierX ? agg_add(&c.cur->qcount) : atomicAdd(&c.cur->qcount, 1u);
   if constexpr (kTier == kTierC) {
     const uint32_t s = (p & ~kErrBit) >> c.gshift;
     if (s >= c.qj) {
@@ -996,8 +1023,9 @@ __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
   SmemPlan p;
   p.ctl_off = align4(sh.rule_words);
   p.aring_off = p.ctl_off + align4(sizeof(Ctl) / 4);
-  p.vring_off = p.aring_off + align4((sh.ring_a * ring_bytes + 3) / 4);
-  p.agents_off = p.vring_off + align4((sh.ring_v * ring_bytes + 3) / 4);
+  const bool smem_rings = tier != kTierX;  // tier X keeps its rings in global memory
+  p.vring_off = p.aring_off + (smem_rings ? align4((sh.ring_a * ring_bytes + 3) / 4) : 0);
+  p.agents_off = p.vring_off + (smem_rings ? align4((sh.ring_v * ring_bytes + 3) / 4) : 0);
   p.outc_off = p.inbox_off = p.mbox_off = 0;
   if (tier == kTierC) {
     p.outc_off = p.agents_off + align4(3 * sizeof(RoundCtr) / 4);
@@ -1797,6 +1825,252 @@ __device__ __forceinline__ void reduce_cluster_body(const NetDesc* __restrict__ 
   if (threadIdx.x == 0 && net < n_nets) sd = nets[net];
   __syncthreads();
   if (net < n_nets) run_net_cluster<kBlock>(sd, sh, pair, rules, smem);
+}
+
+
+// ---------------------------------------------------------------------------
+// Tier X: one net reduced by the whole GPU. Nets too large for a cluster's
+// shared memory (wide L-system nets: 10^5-10^6 redexes per round) keep the
+// single-CTA tier G's global-memory layout, but every CTA of a cooperative
+// grid takes a slice of each round; the round counters, free rings and bump
+// pointers are global (warp-aggregated atomics), and a grid barrier closes
+// the round (its gpu-scope fence also invalidates L1, so agents and queue
+// words written by other SMs in the round are read fresh from L2).
+
+__device__ __forceinline__ void grid_barrier(GridState* g) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t gen = *reinterpret_cast<volatile uint32_t*>(&g->bar_gen);
+    __threadfence();
+    if (atomicAdd(&g->bar_count, 1u) == gridDim.x - 1) {
+      g->bar_count = 0;
+      __threadfence();
+      atomicAdd(&g->bar_gen, 1u);
+    } else {
+      while (*reinterpret_cast<volatile uint32_t*>(&g->bar_gen) == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int kBlock>
+__device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* pair, const uint32_t* rules,
+                             uint32_t* smem) {
+  constexpr int kTier = kTierX;
+  GridState* const g = d.gs;
+  Ctl* const ctl = &g->ctl;
+  Round<kTier> c;
+  c.d = &d;
+  c.ctl = ctl;
+  c.aring = d.g_aring;
+  c.vring = d.g_vring;
+  c.amask = sh.ring_a - 1;
+  c.vmask = sh.ring_v - 1;
+  c.pair = pair;
+  c.rules = rules;
+  c.n_labels = sh.n_labels;
+  c.agents = d.agents;
+  c.vslot = d.vslot;
+  c.cap_agents = d.cap_agents;
+  c.cap_vars = d.cap_vars;
+  c.cap_queue = d.cap_queue;
+  c.cap_def = d.cap_def;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x, gthreads = gridDim.x * kBlock;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const long long clk0 = clock64();
+  const unsigned long long gt0 = globaltimer();
+  const bool fits = d.n_in_agents <= c.cap_agents && d.n_in_vars <= c.cap_vars;
+  // ---- init (the host zeroed the grid state)
+  for (uint32_t i = gtid; i < c.cap_vars; i += gthreads) c.vslot[i] = kNone;
+  if (fits)
+    for (uint32_t i = gtid; i < d.n_in_agents; i += gthreads) c.agents[i] = d.in_agents[i];
+  if (lead) {
+    ctl->agent_bump = d.n_in_agents;
+    ctl->var_bump = d.n_in_vars;
+  }
+  bool stop = false;
+  uint32_t stop_err = 0;
+  if (!fits) {
+    stop = true;
+    stop_err = INET_ERR_ARENA;
+  } else if (d.n_in_eqs == 0) {
+    stop = true;
+    if (lead && d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
+  } else if (sh.max_rounds == 0) {
+    stop = true;
+    stop_err = INET_ERR_LOOP_CAP;
+  }
+  __shared__ uint32_t red3[3];
+  __shared__ uint32_t scan_scratch[34];
+  grid_barrier(g);
+  c.failed = false;
+  uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, rounds = 1;
+  int32_t parked_tot = 0;
+  unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
+  uint2* const Q = d.queue;
+  for (uint32_t r = 1; !stop; ++r) {
+    RoundCtr* cur = &g->ctr3[r % 3];
+    c.cur = cur;
+    c.lo_a = lo_a;
+    c.hi_a = hi_a;
+    c.lo_v = lo_v;
+    c.hi_v = hi_v;
+    c.ints = c.comms = 0;
+    c.parked = 0;
+    c.dout = nullptr;
+    c.out = Q + (r & 1u) * c.cap_queue;
+    if (blockIdx.x == 0 && threadIdx.x < sizeof(RoundCtr) / 4)
+      reinterpret_cast<uint32_t*>(&g->ctr3[(r + 1) % 3])[threadIdx.x] = 0;
+    if (threadIdx.x < 3) red3[threadIdx.x] = 0;
+    if (r == 1) {
+      for (uint32_t b = gtid & ~31u; b < n; b += gthreads) {
+        const uint32_t i = b + lane;
+        const bool v = i < n && !c.failed;
+        const uint2 eq = v ? d.in_eqs[i] : make_uint2(0, 0);
+        const bool act = v && ((eq.x | eq.y) & kVar) == 0;
+        interact_w(c, act, eq.x, eq.y);
+        if (v && !act && !c.failed) link(c, eq.x, eq.y);
+      }
+    } else {
+      const uint2* in = Q + ((r - 1) & 1u) * c.cap_queue;
+      for (uint32_t b = gtid & ~31u; b < n; b += gthreads) {
+        const uint32_t i = b + lane;
+        const bool v = i < n && !c.failed;
+        const uint2 e = v ? in[i] : make_uint2(0, 0);
+        interact_w(c, v, e.x, e.y);
+      }
+    }
+    {
+      const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
+      const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
+      const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
+      __syncthreads();  // red3 cleared
+      if (lane == 0) {
+        if (wi) atomicAdd(&red3[0], wi);
+        if (wc) atomicAdd(&red3[1], wc);
+        if (wp) atomicAdd(&red3[2], static_cast<uint32_t>(wp));
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (red3[0]) atomicAdd(&cur->ints, red3[0]);
+        if (red3[1]) atomicAdd(&cur->comms, red3[1]);
+        if (red3[2]) atomicAdd(&cur->parked, static_cast<int32_t>(red3[2]));
+      }
+    }
+    grid_barrier(g);
+    // ---- close round r (every thread, same values)
+    const RoundCtr k = *cur;
+    const bool round_failed = (k.qcount & kErrBit) != 0;
+    const uint32_t q = k.qcount & ~kErrBit;
+    const uint32_t wa = min(k.afree, sh.ring_a - (hi_a - lo_a));
+    const uint32_t wv = min(k.vfree, sh.ring_v - (hi_v - lo_v));
+    lo_a += min(k.atake, hi_a - lo_a);
+    hi_a += wa;
+    lo_v += min(k.vtake, hi_v - lo_v);
+    hi_v += wv;
+    parked_tot += k.parked;
+    tot_i += k.ints;
+    tot_c += k.comms;
+    if (lead && d.stats) {
+      const unsigned long long now = globaltimer();
+      if (r - 1 < d.cap_rounds)
+        d.stats[r - 1] = make_uint4(k.ints, k.comms, q + static_cast<uint32_t>(parked_tot),
+                                    static_cast<uint32_t>(now - t_prev));
+      t_prev = now;
+    }
+    rounds = r + 1;
+    n = q;
+    if (round_failed) {
+      stop = true;
+    } else if (q == 0) {
+      stop = true;
+      if (lead && d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
+    } else if (sh.detect_vh && k.vh) {
+      stop = true;
+      stop_err = kNeedExact;
+    } else if (r + 1 > sh.max_rounds) {
+      stop = true;
+      stop_err = INET_ERR_LOOP_CAP;
+    } else if (q > c.cap_queue) {
+      stop = true;
+      stop_err = INET_ERR_ARENA;
+    }
+  }
+  if (lead && stop_err) atomicCAS(&ctl->err_code, 0u, stop_err);
+  grid_barrier(g);
+  // ---- results: residual parked equations in variable-id order (two passes)
+  const uint32_t v_hw = min(ctl->var_bump, c.cap_vars), a_hw = min(ctl->agent_bump, c.cap_agents);
+  const uint32_t per = (v_hw + gridDim.x - 1) / gridDim.x;
+  const uint32_t s_lo = min(blockIdx.x * per, v_hw), s_hi = min(s_lo + per, v_hw);
+  uint32_t mine = 0;
+  for (uint32_t x = s_lo + threadIdx.x; x < s_hi; x += kBlock) mine += c.vslot[x] != kNone;
+  mine = __reduce_add_sync(0xFFFFFFFFu, mine);
+  if (threadIdx.x == 0) red3[0] = 0;
+  __syncthreads();
+  if (lane == 0 && mine) atomicAdd(&red3[0], mine);
+  __syncthreads();
+  if (threadIdx.x == 0) g->blk_res[blockIdx.x] = red3[0];
+  grid_barrier(g);
+  uint32_t base = 0, n_res = 0;
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) {
+    const uint32_t v = g->blk_res[b];
+    n_res += v;
+    if (b < blockIdx.x) base += v;
+  }
+  // block-wide sums of base / n_res
+  base = __reduce_add_sync(0xFFFFFFFFu, base);
+  n_res = __reduce_add_sync(0xFFFFFFFFu, n_res);
+  __shared__ uint32_t sums[2][32];
+  if (lane == 0) {
+    sums[0][warp] = base;
+    sums[1][warp] = n_res;
+  }
+  __syncthreads();
+  base = 0;
+  n_res = 0;
+  for (uint32_t w = 0; w < kBlock / 32; ++w) {
+    base += sums[0][w];
+    n_res += sums[1][w];
+  }
+  __syncthreads();
+  for (uint32_t c0 = s_lo; c0 < s_hi; c0 += kBlock) {
+    const uint32_t x = c0 + threadIdx.x;
+    const uint32_t v = x < s_hi ? c.vslot[x] : kNone;
+    uint32_t off;
+    const uint32_t tot = block_scan_flag(v != kNone, scan_scratch, &off);
+    if (v != kNone && base + off < d.cap_vars) d.residual[base + off] = make_uint2(kVar | x, v);
+    base += tot;
+  }
+  if (lead) {
+    NetCtl* o = d.ctl;
+    o->agent_bump = a_hw;
+    o->var_bump = v_hw;
+    o->err = ctl->err_code;
+    o->err_a = ctl->err_a;
+    o->err_b = ctl->err_b;
+    o->rounds = rounds;
+    o->interactions = tot_i;
+    o->communications = tot_c;
+    o->n_residual = n_res;
+    o->parked_total = static_cast<uint32_t>(parked_tot);
+    o->pad[0] = clock_mhz(clk0, gt0);
+    if ((ctl->agent_bump > d.cap_agents || ctl->var_bump > d.cap_vars) && o->err == 0) o->err = INET_ERR_ARENA;
+  }
+}
+
+template <int kBlock>
+__device__ __forceinline__ void reduce_grid_body(const NetDesc* __restrict__ nets, uint32_t n_nets,
+                                                 const uint32_t* __restrict__ blob, const Shape& sh, uint32_t* smem,
+                                                 NetDesc& sd) {
+  for (uint32_t i = threadIdx.x; i < sh.rule_words; i += kBlock) smem[i] = blob[4 + i];
+  const uint32_t pair_words = (sh.n_labels * sh.n_labels + 1) / 2;
+  const uint16_t* pair = reinterpret_cast<const uint16_t*>(smem);
+  const uint32_t* rules = smem + pair_words;
+  if (threadIdx.x == 0) sd = nets[0];
+  __syncthreads();
+  if (n_nets >= 1) run_net_grid<kBlock>(sd, sh, pair, rules, smem);
 }
 
 }  // namespace inetdev

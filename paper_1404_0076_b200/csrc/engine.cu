@@ -51,6 +51,14 @@ __global__ void __launch_bounds__(kBlock) reduce_cluster_kernel(const NetDesc* _
   inetdev::reduce_cluster_body<kBlock>(nets, n_nets, blob, sh, smem, sd);
 }
 
+template <int kBlock>
+__global__ void __launch_bounds__(kBlock) reduce_grid_kernel(const NetDesc* __restrict__ nets, uint32_t n_nets,
+                                                             const uint32_t* __restrict__ blob, Shape sh) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ NetDesc sd;
+  inetdev::reduce_grid_body<kBlock>(nets, n_nets, blob, sh, smem, sd);
+}
+
 using KernelFn = void (*)(const NetDesc*, uint32_t, const uint32_t*, Shape);
 
 KernelFn pick_cluster_kernel(uint32_t threads) {
@@ -86,6 +94,7 @@ KernelFn pick_kernel_t(uint32_t threads) {
 
 KernelFn pick_kernel(uint32_t threads, int tier) {
   if (tier == kTierC) return pick_cluster_kernel(threads);
+  if (tier == inetdev::kTierX) return threads <= 256 ? reduce_grid_kernel<256> : reduce_grid_kernel<512>;
   if (tier == kTierS) return pick_kernel_t<kTierS>(threads);
   if (tier == kTierM) return pick_kernel_t<kTierM>(threads);
   return pick_kernel_t<kTierG>(threads);
@@ -167,7 +176,8 @@ struct inet_ctx {
   bool input_resident = false;
   // device state
   DevBuf d_in_agents, d_in_eqs, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist,
-      d_defer;
+      d_defer, d_gs;
+  bool grid_tier = false;  // the next layout is for tier X (global rings + grid state)
   uint32_t cap_def = 0;  // deferred equations per net and round (reference loop mode)
   bool count_rules = false;
   std::vector<uint32_t> h_hist;
@@ -278,7 +288,7 @@ void inet_ctx_destroy(inet_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->d_blob, &c->d_in_agents, &c->d_in_eqs, &c->d_desc, &c->d_agents, &c->d_vslot, &c->d_aring,
-                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer})
+                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer, &c->d_gs})
     b->release();
   for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -377,8 +387,11 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
       c->d_ctl.ensure(N * sizeof(NetCtl)) || c->d_desc.ensure(N * sizeof(NetDesc)) ||
       (cap_rounds && c->d_stats.ensure(N * cap_rounds * 16)) ||
       (c->count_rules && c->d_hist.ensure(N * hist_stride(c) * 4)) ||
-      (c->cap_def && c->d_defer.ensure(N * 2 * c->cap_def * 8)))
+      (c->cap_def && c->d_defer.ensure(N * 2 * c->cap_def * 8)) ||
+      (c->grid_tier && (c->d_aring.ensure(size_t(cap_agents) * 4) || c->d_vring.ensure(size_t(cap_vars) * 4) ||
+                        c->d_gs.ensure(sizeof(inetdev::GridState) + 4096 * 4))))
     return INET_ERR_CUDA;
+  if (c->grid_tier) CUDA_TRY(cudaMemsetAsync(c->d_gs.p, 0, sizeof(inetdev::GridState) + 4096 * 4, c->stream));
   if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * hist_stride(c) * 4, c->stream));
   std::vector<NetDesc> desc(n);
   for (uint32_t i = 0; i < n; ++i) {
@@ -395,6 +408,11 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.cap_vars = cap_vars;
     d.cap_queue = cap_queue;
     d.cap_rounds = cap_rounds;
+    if (c->grid_tier) {
+      d.g_aring = static_cast<uint32_t*>(c->d_aring.p);
+      d.g_vring = static_cast<uint32_t*>(c->d_vring.p);
+      d.gs = static_cast<inetdev::GridState*>(c->d_gs.p);
+    }
     d.deferred = c->cap_def ? static_cast<uint2*>(c->d_defer.p) + size_t(i) * 2 * c->cap_def : nullptr;
     d.cap_def = c->cap_def;
     d.in_agents = static_cast<const uint4*>(c->d_in_agents.p) + c->agent_off[i];
@@ -452,7 +470,7 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
   if (!c->jit_mode) return nullptr;
   // code style per tier: straight-line cases where the rewrite is issue-bound
   // (S, M, G); a uniform memory phase where remote latency dominates (C)
-  const int style = c->jit_style >= 0 ? c->jit_style : (tier == kTierC ? 1 : 0);
+  const int style = c->jit_style >= 0 ? c->jit_style : (tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0);
   const auto key = std::make_tuple(tier, threads, style + (c->exact_code ? 16 : 0));
   auto it = c->jit_kernels.find(key);
   if (it != c->jit_kernels.end()) return reinterpret_cast<const void*>(it->second.second);
@@ -477,7 +495,7 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
 }
 
 int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
-  const uint32_t threads = tier == kTierC ? cluster_threads(cfg) : auto_threads(c, cfg);
+  const uint32_t threads = tier == kTierC ? cluster_threads(cfg) : tier == inetdev::kTierX ? 256u : auto_threads(c, cfg);
   sh.threads = threads;
   const void* jk = jit_kernel(c, tier, threads);
   const void* fn = jk ? jk : reinterpret_cast<const void*>(pick_kernel(threads, tier));
@@ -515,6 +533,20 @@ int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
     }
     CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
     CUDA_TRY(cudaLaunchKernelExC(&lc, fn, args));
+  } else if (tier == inetdev::kTierX) {
+    // the whole GPU on one net: every CTA resident (cooperative launch)
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), smem);
+    if (per_sm < 1) return INET_ERR_UNSUPPORTED;
+    const uint32_t grid = std::min<uint32_t>(uint32_t(dev_sms) * uint32_t(per_sm), 4096u);
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, c->stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      if (std::getenv("INET_B200_DEBUG"))
+        std::fprintf(stderr, "inet_b200: tier X launch failed (%s), grid %u\n", cudaGetErrorString(e), grid);
+      return INET_ERR_UNSUPPORTED;
+    }
   } else {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(threads), smem);
@@ -671,7 +703,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
       }
     }
   }
-  if (!done && want_g >= 2 && c->n_nets <= 64) {
+  if (!done && want_g >= 2 && want_g <= 16 && c->n_nets <= 64) {
     uint32_t G = 2;  // a power of two (ids are owned round-robin: owner = id & (G - 1))
     while (G * 2 <= std::min<uint32_t>(want_g, 16)) G *= 2;
     Shape sh = base_shape(c, max_loops);
@@ -687,6 +719,34 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     if (!done) {
       c->resume.on = false;  // the single-CTA tiers below start over from the input
       c->promoted = false;
+    }
+  }
+  // Single nets too large for a cluster (or ctas_per_net > 16): the whole GPU
+  // (tier X), capacities doubled on overflow.
+  if (!done && c->n_nets == 1 && (cfg ? cfg->ctas_per_net : 0) != 1) {
+    uint32_t ca = cfg && cfg->cap_agents ? cfg->cap_agents : (1u << 20);
+    uint32_t cv = cfg && cfg->cap_vars ? cfg->cap_vars : (1u << 20);
+    ca = std::max(ca, c->max_in_agents + 64);
+    cv = std::max(cv, c->max_in_vars + 64);
+    for (uint32_t attempt = 0; !done; ++attempt) {
+      uint32_t ra = 1, rv = 1;
+      while (ra < ca) ra *= 2;
+      while (rv < cv) rv *= 2;
+      Shape sh = base_shape(c, max_loops);
+      sh.ring_a = ra;
+      sh.ring_v = rv;
+      c->grid_tier = true;
+      int st = attempt_tier(inetdev::kTierX, sh, ra, rv, ra / 2 + 1);
+      c->grid_tier = false;
+      if (st == INET_ERR_UNSUPPORTED) break;
+      if (st) return st;
+      if (!any_oom()) {
+        done = true;
+        break;
+      }
+      if (attempt + 1 >= retries || uint64_t(ra) * 2 >= INET_VAR_BIT) break;
+      ca = ra * 2;
+      cv = rv * 2;
     }
   }
   if (!done && !user_caps && c->n_nets <= 148 && c->max_in_agents < 32768 && c->max_in_vars < 16384) {
@@ -830,7 +890,9 @@ int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
     c->cap_vars = cv;
     c->cap_queue = cq;
   }
+  c->grid_tier = c->tier == inetdev::kTierX;
   int st = layout(c, c->cap_agents, c->cap_vars, c->cap_queue, cap_rounds);
+  c->grid_tier = false;
   if (st) return st;
   Shape sh = c->shape;
   sh.max_rounds = k.max_loops;

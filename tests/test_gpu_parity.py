@@ -299,3 +299,35 @@ def test_both_loop_modes_reach_the_same_normal_form(exact):
     assert res.total_interactions == 50_515
     assert programs.nat_value(res.final.interface[0]) == 2584
     _check_loops(res)
+
+
+# ---- tier X: one net on the whole GPU (cooperative grid, global memory) -------
+
+def test_whole_gpu_tier_fixtures():
+    """Every reference fixture forced through the whole-GPU tier (ctas_per_net > 16)."""
+    for case in CASES:
+        config, rules = _case_inputs(case)
+        kw = dict(case.get("engine_config", {}))
+        kw["ctas_per_net"] = 148
+        cfg = EngineConfig(**kw)
+        if "error" in case:
+            with pytest.raises(getattr(errors, case["error"])):
+                evaluate(config, rules, cfg)
+            continue
+        res = evaluate(config, rules, cfg)
+        assert res.total_interactions == case["interactions"], case["name"]
+        assert _sha(print_configuration(res.final)) == case["print_sha256"], case["name"]
+        _check_loops(res)
+
+
+@pytest.mark.parametrize("n", [22, 24])
+def test_wide_lsystem_against_oracle(n):
+    """L-system nets too wide for a cluster run on the whole GPU; same result as the oracle."""
+    prog = programs.program("lsystem")
+    net = prog.build_input(n)
+    res = evaluate(net, prog.rules)
+    want = O.run_config(net, O.rules_for("lsystem"), collect=True)
+    assert res.total_interactions == want.interactions
+    assert print_configuration(res.final) == want.printed()
+    assert len(res.loops) == want.loops
+    assert [s.interactions for s in res.loops] == [row[0] for row in want.rows]
