@@ -447,7 +447,9 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
     if (t <= 512) return 512;
     return 1024;
   }
-  if (c->n_nets >= 2048) return 128;
+  // measured on 4096/1024/512/256 x A(3,6): 128 threads once there are about
+  // as many nets as SMs x 7, 256 below that
+  if (c->n_nets >= 1024) return 128;
   if (c->n_nets >= 256) return 256;
   return c->n_nets >= 16 ? 512 : 1024;
 }
