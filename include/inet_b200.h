@@ -114,9 +114,11 @@ typedef struct inet_net_stats {
   uint32_t n_residual;     /* parked equations at the fixpoint (input of finalize) */
   uint32_t cap_agents;     /* capacities the successful run used */
   uint32_t cap_vars;
-  uint32_t tier;           /* residency tier used: 0 S (shared), 1 M (mixed), 2 G (global) */
+  uint32_t tier;           /* residency tier used: 0 S (shared), 1 M (mixed), 2 G (global), 3 C (cluster), 4 X (whole GPU) */
   uint32_t jit;            /* 1 if the rule-set specialised kernel ran (else the interpreter) */
   uint32_t sm_mhz;         /* effective SM clock over this net's reduction (clock64 / globaltimer) */
+  uint32_t device_final;   /* 1 if the normal form was finalized on the device (tier S), else the host did */
+  uint32_t reserved;
 } inet_net_stats;
 
 /* Context: one device, one stream, device buffers reused across calls.

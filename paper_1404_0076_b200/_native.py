@@ -73,6 +73,8 @@ class NetStats(C.Structure):
         ("tier", C.c_uint32),
         ("jit", C.c_uint32),
         ("sm_mhz", C.c_uint32),
+        ("device_final", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 

@@ -204,6 +204,9 @@ struct NetDesc {
   uint32_t* g_aring;
   uint32_t* g_vring;
   struct GridState* gs;
+  // device-side finalize (tier S): the net's interface; dev_final enables it
+  const uint32_t* in_iface;
+  uint32_t n_iface, dev_final;
 };
 
 // Launch-wide shape: ring sizes and the shared-memory capacities.
@@ -1047,6 +1050,107 @@ __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
   return p;
 }
 
+// Device-side finalize of a tier S net whose arena is still in shared memory
+// (restates engine.finalize, src/inet/engine.py:287-362, and the preorder
+// compaction of host.cpp finalize_net, for the nets where every parked
+// equation is eliminated). A parked equation x = t (slot[x] = t) has the
+// other occurrence of x in the interface or in an agent port; walking the net
+// from the interface roots in preorder (port 0 first), every variable met
+// whose slot is set is replaced by its value (following var-valued chains), so
+// each equation is consumed at its variable's other occurrence exactly as the
+// reference's elimination does. When the walk consumes every parked equation
+// the substituted net is a tree whose preorder is the host's compaction order:
+// records go to d.agents[0, nf), the interface to d.residual[i].x, and nf + 1
+// is returned. Otherwise (an equation left over: a cycle or a part not
+// reachable from the interface; a shared agent; an interface longer than 32;
+// scratch that does not fit) nothing is written and 0 is returned: the host
+// finalizes from the arena copy as before.
+// Scratch, all free once the loop has stopped: the queues hold the DFS stack,
+// the agent ring the preorder list, the variable ring the remap table.
+constexpr uint32_t kConsumed = 0x40000000u;  // finalize_smem: a parked equation already applied
+
+template <int kTier>
+__device__ uint32_t finalize_smem(const Round<kTier>& c, const NetDesc& d, Ctl* ctl, const SmemPlan& plan,
+                                  uint32_t* smem, const Shape& sh, uint32_t hw, uint32_t ahw, uint32_t n_parked) {
+  uint32_t* const ifc = ctl->scratch;  // the resolved interface (<= 32 refs); scratch[33]: verdict
+  uint32_t* const stack = smem + plan.queue_off;
+  uint16_t* const order = reinterpret_cast<uint16_t*>(smem + plan.aring_off);
+  uint16_t* const remap = reinterpret_cast<uint16_t*>(smem + plan.vring_off);
+  const uint32_t ni = d.n_iface;
+  const bool fits = ctl->err_code == 0 && ni <= 32 && 2 * sh.res_queue >= ahw + 3 && sh.ring_a >= ahw &&
+                    sh.ring_v >= ahw && ahw < 0xFFFFu;
+  __syncthreads();  // the residual scan's last use of ctl->scratch
+  if (!fits) return 0;
+  for (uint32_t i = threadIdx.x; i < ahw; i += blockDim.x) remap[i] = 0xFFFFu;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t consumed = 0, nf = 0, sp = 0;
+    bool ok = true;
+    // the value a reference stands for once the parked equations are applied;
+    // a consumed slot keeps its value, marked (a variable is met at most once)
+    auto resolve = [&](uint32_t t) {
+      for (uint32_t guard = 0; t != kNone && (t & kVar) && guard <= n_parked; ++guard) {
+        const uint32_t x = t & ~kVar;
+        const uint32_t v = x < hw ? c.vslot[x] : kNone;
+        if (v == kNone) break;
+        if (v & kConsumed) {
+          ok = false;
+          break;
+        }
+        c.vslot[x] = v | kConsumed;
+        consumed += 1;
+        t = v;
+      }
+      return t;
+    };
+    for (uint32_t i = 0; i < ni && ok; ++i) {
+      const uint32_t root = resolve(d.in_iface[i]);
+      ifc[i] = root;
+      if (root == kNone || (root & kVar)) continue;
+      stack[sp++] = root;
+      while (sp) {
+        const uint32_t a = stack[--sp];
+        if (a >= ahw || remap[a] != 0xFFFFu) {  // shared agent: not a tree
+          ok = false;
+          break;
+        }
+        remap[a] = static_cast<uint16_t>(nf);
+        order[nf++] = static_cast<uint16_t>(a);
+        const uint4 A = ld_agent(c, a);
+        const uint4 R = make_uint4(A.x, resolve(A.y), resolve(A.z), resolve(A.w));
+        if (sp + 3 > 2 * sh.res_queue) {
+          ok = false;
+          break;
+        }
+        if (R.w != kNone && !(R.w & kVar)) stack[sp++] = R.w;
+        if (R.z != kNone && !(R.z & kVar)) stack[sp++] = R.z;
+        if (R.y != kNone && !(R.y & kVar)) stack[sp++] = R.y;
+      }
+    }
+    ctl->scratch[33] = ok && consumed == n_parked ? nf + 1 : 0u;
+  }
+  __syncthreads();
+  const uint32_t rows = ctl->scratch[33];
+  if (!rows) return 0;
+  // the agents themselves are left untouched (a failed attempt must leave the
+  // arena as the host finalize expects it): ports are resolved again here
+  auto map = [&](uint32_t t) {
+    for (uint32_t guard = 0; t != kNone && (t & kVar) && guard <= n_parked; ++guard) {
+      const uint32_t x = t & ~kVar;
+      const uint32_t v = x < hw ? c.vslot[x] : kNone;
+      if (v == kNone) break;
+      t = v & ~kConsumed;
+    }
+    return (t == kNone || (t & kVar)) ? t : static_cast<uint32_t>(remap[t]);
+  };
+  for (uint32_t j = threadIdx.x; j < rows - 1; j += blockDim.x) {
+    const uint4 A = ld_agent(c, order[j]);
+    d.agents[j] = make_uint4(A.x, map(A.y), map(A.z), map(A.w));
+  }
+  if (threadIdx.x < ni) d.residual[threadIdx.x] = make_uint2(map(ifc[threadIdx.x]), 0u);
+  return rows;
+}
+
 // Reduce one net to its fixpoint; the whole CTA cooperates.
 template <int kTier>
 __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair, const uint32_t* rules,
@@ -1318,8 +1422,12 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     base += tot;
   }
   const uint32_t ahw = min(ctl->agent_bump, c.cap_agents);
+  uint32_t nf_rows = 0;  // device-finalized normal form: agents + 1 (0: the host finalizes)
+  if constexpr (kTier == kTierS) {
+    if (d.dev_final && !handed) nf_rows = finalize_smem(c, d, ctl, plan, smem, sh, hw, ahw, base);
+  }
   if constexpr (T::kAgentsSmem) {
-    const uint32_t n_copy = min(ahw, d.cap_agents);
+    const uint32_t n_copy = nf_rows ? 0u : min(ahw, d.cap_agents);
     for (uint32_t i = threadIdx.x; i < n_copy; i += blockDim.x) d.agents[i] = ld_agent(c, i);
   }
   if (threadIdx.x == 0) {
@@ -1335,6 +1443,8 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     g->n_residual = base;
     g->parked_total = static_cast<uint32_t>(ctl->parked_total);
     g->pad[0] = clock_mhz(clk0, gt0);
+    g->pad[1] = nf_rows;
+    g->pad[2] = nf_rows ? d.n_iface : 0u;
     if ((ahw > d.cap_agents || hw > d.cap_vars) && g->err == 0) g->err = INET_ERR_ARENA;
   }
   __syncthreads();

@@ -175,7 +175,7 @@ struct inet_ctx {
   uint32_t max_in_agents = 0, max_in_eqs = 0, max_in_vars = 0;
   bool input_resident = false;
   // device state
-  DevBuf d_in_agents, d_in_eqs, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist,
+  DevBuf d_in_agents, d_in_eqs, d_in_iface, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist,
       d_defer, d_gs;
   bool grid_tier = false;  // the next layout is for tier X (global rings + grid state)
   uint32_t cap_def = 0;  // deferred equations per net and round (reference loop mode)
@@ -217,6 +217,8 @@ struct inet_ctx {
   std::string jit_log;
   std::map<std::tuple<int, uint32_t, int>, std::pair<cudaLibrary_t, cudaKernel_t>> jit_kernels;
   int jit_style = -1;  // -1: per tier (measured defaults); env INET_B200_JITSTYLE overrides
+  bool dev_final = true;  // tier S finalizes nets on the device; env INET_B200_DEVFINAL=0 disables
+  std::vector<uint32_t> dev_rows;  // per net: device-finalized normal-form agents + 1 (0: host finalize)
   bool exact_code = true;  // rule-set kernel variant with reference-loop (deferred equation) code
 };
 
@@ -275,6 +277,7 @@ int inet_ctx_create(int device, inet_ctx** out) {
   if (const char* e = std::getenv("INET_B200_JIT")) c->jit_mode = std::atoi(e);
   if (const char* e = std::getenv("INET_B200_JITSTYLE")) c->jit_style = std::atoi(e);
   if (const char* e = std::getenv("INET_B200_PROMOTE")) c->promote_ints = static_cast<uint32_t>(std::atol(e));
+  if (const char* e = std::getenv("INET_B200_DEVFINAL")) c->dev_final = std::atoi(e) != 0;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
     delete c;
@@ -364,13 +367,15 @@ int inet_batch_load(inet_ctx* c, uint32_t n_nets, const uint32_t* agents, const 
 namespace {
 
 int upload_input(inet_ctx* c) {
-  const size_t na = c->agents.size() * 4, ne = c->eqs.size() * 4;
-  if (c->d_in_agents.ensure(std::max<size_t>(na, 16)) || c->d_in_eqs.ensure(std::max<size_t>(ne, 8)))
+  const size_t na = c->agents.size() * 4, ne = c->eqs.size() * 4, ni = c->iface.size() * 4;
+  if (c->d_in_agents.ensure(std::max<size_t>(na, 16)) || c->d_in_eqs.ensure(std::max<size_t>(ne, 8)) ||
+      c->d_in_iface.ensure(std::max<size_t>(ni, 4)))
     return INET_ERR_CUDA;
   if (na) CUDA_TRY(cudaMemcpyAsync(c->d_in_agents.p, c->agents.data(), na, cudaMemcpyHostToDevice, c->stream));
   if (ne) CUDA_TRY(cudaMemcpyAsync(c->d_in_eqs.p, c->eqs.data(), ne, cudaMemcpyHostToDevice, c->stream));
+  if (ni) CUDA_TRY(cudaMemcpyAsync(c->d_in_iface.p, c->iface.data(), ni, cudaMemcpyHostToDevice, c->stream));
   c->input_resident = true;
-  c->io_h2d += na + ne;
+  c->io_h2d += na + ne + ni;
   return INET_OK;
 }
 
@@ -420,6 +425,9 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.n_in_agents = static_cast<uint32_t>(c->agent_off[i + 1] - c->agent_off[i]);
     d.n_in_eqs = static_cast<uint32_t>(c->eq_off[i + 1] - c->eq_off[i]);
     d.n_in_vars = c->n_vars[i];
+    d.in_iface = static_cast<const uint32_t*>(c->d_in_iface.p) + c->iface_off[i];
+    d.n_iface = static_cast<uint32_t>(c->iface_off[i + 1] - c->iface_off[i]);
+    d.dev_final = c->dev_final ? 1u : 0u;
     if (c->resume.on && n == 1) {
       // resume from tier M's hand-over: its arena, slot table and pending equations
       d.in_agents = d.agents;
@@ -787,9 +795,11 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   if (c->promoted && c->tier != kTierC) c->promoted = false;  // the cluster fell through: no prefix
   if (device_ms) *device_ms = ms + (c->promoted ? c->promo_ms : 0.0f);
   c->stats.assign(c->n_nets, inet_net_stats{});
+  c->dev_rows.assign(c->n_nets, 0);
   int first = INET_OK;
   for (uint32_t i = 0; i < c->n_nets; ++i) {
     const NetCtl& k = c->ctl[i];
+    if (c->tier == kTierS && k.err == 0) c->dev_rows[i] = k.pad[1];
     inet_net_stats& s = c->stats[i];
     s.interactions = k.interactions;
     s.communications = k.communications;
@@ -805,6 +815,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     s.tier = static_cast<uint32_t>(c->tier);
     s.jit = c->last_jit ? 1u : 0u;
     s.sm_mhz = k.pad[0];
+    s.device_final = c->dev_rows[i] ? 1u : 0u;
     if (first == INET_OK && k.err) first = static_cast<int>(k.err);
   }
   c->reduced = true;
@@ -812,10 +823,13 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   c->finalized.assign(c->n_nets, 0);
   if (fetch) {
     // results: agent slabs up to the high-water, residual equations, round rows
+    // (nets finalized on the device: their compacted normal form and interface)
     uint32_t max_hw = 0, max_res = 0;
-    for (auto& s : c->stats) {
-      max_hw = std::max(max_hw, s.agent_hw);
-      max_res = std::max(max_res, s.n_residual);
+    for (uint32_t i = 0; i < c->n_nets; ++i) {
+      const inet_net_stats& s = c->stats[i];
+      const bool dev = c->dev_rows[i] != 0;
+      max_hw = std::max(max_hw, dev ? c->dev_rows[i] - 1 : s.agent_hw);
+      max_res = std::max(max_res, dev ? c->ctl[i].pad[2] : s.n_residual);
     }
     // strided copies of each slab's used prefix
     c->agent_pitch = std::max(max_hw, 1u);
@@ -1046,6 +1060,19 @@ int finalize_batch(inet_ctx& c, uint32_t net, uint32_t n_threads) {
   auto one = [&](uint32_t i) -> int {
     const inet_net_stats& s = c.stats[i];
     if (s.status != INET_OK) return static_cast<int>(s.status);
+    if (const uint32_t rows = i < c.dev_rows.size() ? c.dev_rows[i] : 0u) {
+      // finalized on the device: copy out the compacted normal form
+      NormalForm& nf = c.results[i];
+      const uint32_t* ag = c.h_agents.data() + size_t(i) * c.agent_pitch * 4;
+      const uint32_t* rs = c.h_resid.data() + size_t(i) * c.resid_pitch * 2;
+      const uint32_t ni = static_cast<uint32_t>(c.iface_off[i + 1] - c.iface_off[i]);
+      nf.agents.assign(ag, ag + size_t(rows - 1) * 4);
+      nf.iface.resize(ni);
+      for (uint32_t k = 0; k < ni; ++k) nf.iface[k] = rs[2 * k];
+      nf.eqs.clear();
+      c.finalized[i] = 1;
+      return INET_OK;
+    }
     NetView v;
     v.agents = c.h_agents.data() + size_t(i) * c.agent_pitch * 4;
     v.n_agents = s.agent_hw;

@@ -1,0 +1,100 @@
+"""Device-side finalize (tier S): the compacted normal form written by the
+kernel equals the host finalize of the same reduction, array for array, and
+the nets it cannot handle fall back to the host."""
+
+import os
+import random
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1404_0076_b200 import EngineConfig, _native, engine, print_configuration
+from paper_1404_0076_b200 import programs
+from paper_1404_0076_b200.flat import unflatten
+
+from test_gpu_parity import _random_arith_net
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(dev_final):
+    old = os.environ.get("INET_B200_DEVFINAL")
+    os.environ["INET_B200_DEVFINAL"] = "1" if dev_final else "0"
+    try:
+        return _native.Context(0)
+    finally:
+        if old is None:
+            del os.environ["INET_B200_DEVFINAL"]
+        else:
+            os.environ["INET_B200_DEVFINAL"] = old
+
+
+def _reduce(ctx, nets, rules):
+    prep = engine.prepare(nets, rules)
+    code, _ = engine.run_prepared(ctx, prep, EngineConfig(collect_stats=False))
+    assert code == _native.OK
+    assert ctx.finalize(0xFFFFFFFF, 0) == _native.OK
+    out = []
+    for i in range(len(nets)):
+        st = ctx.stats(i)
+        agents, iface, eqs = ctx.result(i)
+        out.append((st, np.array(agents, copy=True), np.array(iface, copy=True), np.array(eqs, copy=True)))
+    return prep, out
+
+
+def _compare(nets, rules, orules=None, want_device=None):
+    dev = _ctx(True)
+    host = _ctx(False)
+    try:
+        prep, got = _reduce(dev, nets, rules)
+        _, ref = _reduce(host, nets, rules)
+    finally:
+        dev.close()
+        host.close()
+    n_dev = 0
+    for i, ((sd, ad, idf, ed), (sh, ah, ih, eh)) in enumerate(zip(got, ref)):
+        assert sd.tier == 0, "these batches must run in tier S"
+        assert sh.device_final == 0
+        n_dev += sd.device_final
+        assert sd.interactions == sh.interactions
+        assert np.array_equal(ad, ah), i
+        assert np.array_equal(idf, ih), i
+        assert np.array_equal(ed, eh), i
+        if orules is not None and i < 64:
+            final = unflatten(ad, idf, ed, prep.labels, prep.flats[i], engine.term_classes(nets[i]))
+            assert print_configuration(final) == O.run_config(nets[i], orules, collect=False).printed()
+    if want_device is not None:
+        assert n_dev == want_device
+    return n_dev
+
+
+def test_ackermann_batch_finalized_on_device():
+    prog = programs.program("ackermann")
+    rng = random.Random(3)
+    params = [(rng.randint(0, 3), rng.randint(0, 5)) for _ in range(300)]
+    nets = [prog.build_input(m, n) for m, n in params]
+    # every Ackermann result is one parked equation x = S(...S(Z)) with x the interface
+    _compare(nets, prog.rules, O.rules_for("ackermann"), want_device=len(nets))
+
+
+def test_random_arith_batch_device_and_host_paths():
+    rules = programs.load_rules("arith")
+    rng = random.Random(99)
+    nets = [_random_arith_net(rng, rules.symbols, rng.choice([8, 40, 200])) for _ in range(200)]
+    n_dev = _compare(nets, rules, O.rules_for("arith"))
+    assert n_dev > 0
+
+
+def test_interface_variables_fall_back_to_host():
+    # x and y wired straight through (x = y): a var-valued parked equation,
+    # finalized by the host; a closed result next to it stays on the device
+    from paper_1404_0076_b200 import Agent, Configuration, Equation, Var
+
+    prog = programs.program("ackermann")
+    syms = prog.rules.symbols
+    wire = Configuration((Var(0), Var(1)), (Equation(Var(0), Var(1)),))
+    closed = prog.build_input(2, 2)
+    pair = Configuration((Var(0),), (Equation(Var(0), Agent(syms["Z"])),))
+    nets = [wire, closed, pair, wire, closed]
+    _compare(nets, prog.rules)
