@@ -1232,6 +1232,12 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
 #endif
   const uint32_t lane = threadIdx.x & 31u;
   c.cap_def = d.cap_def;
+  // Per-round totals are only needed for the per-round rows and tier M's
+  // hand-over threshold; otherwise each thread keeps its own running totals,
+  // summed once after the loop.
+  const bool per_round = d.stats != nullptr || (kTier == kTierM && sh.promote_ints != 0);
+  c.ints = c.comms = 0;
+  c.parked = 0;
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, nd = 0, rounds = 1;
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
@@ -1242,8 +1248,10 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     c.hi_a = hi_a;
     c.lo_v = lo_v;
     c.hi_v = hi_v;
-    c.ints = c.comms = 0;
-    c.parked = 0;
+    if (per_round) {
+      c.ints = c.comms = 0;
+      c.parked = 0;
+    }
     if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(&ctl->ctr3[(r + 1) % 3])[threadIdx.x] = 0;
     c.dout = sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
     c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + (r & 1u) * qstride)
@@ -1314,7 +1322,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       }
     }
     INET_TMARK(c, 5);
-    {
+    if (per_round) {
       const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
       const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
       const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
@@ -1387,6 +1395,17 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     ctl->parked_total = parked_tot;
     ctl->hdr.n = n;
     ctl->hdr.nd = nd;
+  }
+  if (!per_round) {
+    __syncthreads();
+    const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
+    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
+    const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
+    if (lane == 0) {
+      if (wi) atomicAdd(&ctl->tot_i, static_cast<unsigned long long>(wi));
+      if (wc) atomicAdd(&ctl->tot_c, static_cast<unsigned long long>(wc));
+      if (wp) atomicAdd(&ctl->parked_total, wp);
+    }
   }
 #ifdef INET_TIMING
   if (d.rule_hist)
