@@ -352,7 +352,7 @@ def run_ours(args) -> None:
             "config": dict(wl, parallelism=f"dp{world} (nets sharded, no collective)",
                            interactions_per_net=per_net, rounds_per_net=max_rounds,
                            threads_per_net=engine.native_cfg(ecfg).threads or "auto",
-                           tier="SMG"[ctx.stats(0).tier], agent_hw=ctx.stats(0).agent_hw,
+                           tier="SMGCX"[ctx.stats(0).tier], agent_hw=ctx.stats(0).agent_hw,
                            var_hw=ctx.stats(0).var_hw),
             "e2e": {"value": e2e_value, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
