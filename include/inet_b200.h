@@ -216,6 +216,23 @@ int inet_batch_result(inet_ctx* ctx, uint32_t net, const uint32_t** agents, uint
 int inet_finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface, uint32_t* eqs,
                        uint32_t n_eqs, uint32_t n_vars, uint8_t* alive);
 
+/*
+ * Canonical text of a normal form: lang.print_configuration (src/inet/lang.py:
+ * 333-396) — equations oriented by structural skeleton (lang.py:347-365) and
+ * stably sorted, variables renamed x0, x1, ... in first-occurrence preorder
+ * (core.iter_vars, core.py:96-104). names[l] / arity[l] describe label l (the
+ * rule blob's numbering). Writes min(cap, len) bytes (no terminating NUL) and
+ * the full length to *len; call again with a larger buffer when *len > cap.
+ * inet_print_flat prints flat arrays in the inet_batch_result layout (agents in
+ * any order, refs index the agent array); inet_batch_print prints a finalized
+ * net of the context without building terms on the host.
+ */
+int inet_print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface, uint32_t n_iface,
+                    const uint32_t* eqs, uint32_t n_eqs, const char* const* names, const uint8_t* arity,
+                    uint32_t n_labels, char* buf, size_t cap, size_t* len);
+int inet_batch_print(inet_ctx* ctx, uint32_t net, const char* const* names, const uint8_t* arity,
+                     uint32_t n_labels, char* buf, size_t cap, size_t* len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,7 @@ from .engine import (
     evaluate,
     evaluate_batch,
     evaluate_sharded,
+    evaluate_text,
     finalize,
     reduce_by_key,
 )
@@ -55,6 +56,7 @@ __all__ = [
     "evaluate",
     "evaluate_batch",
     "evaluate_sharded",
+    "evaluate_text",
     "finalize",
     "find_rule",
     "parse_program",

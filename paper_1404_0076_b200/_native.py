@@ -40,6 +40,8 @@ EXPORTS = (
     "inet_batch_finalize",
     "inet_batch_result",
     "inet_finalize_flat",
+    "inet_print_flat",
+    "inet_batch_print",
 )
 
 
@@ -119,6 +121,16 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             "inet_finalize_flat": (
                 C.c_int,
                 [_u32p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8)],
+            ),
+            "inet_print_flat": (
+                C.c_int,
+                [_u32p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32, C.POINTER(C.c_char_p),
+                 C.POINTER(C.c_uint8), C.c_uint32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+            ),
+            "inet_batch_print": (
+                C.c_int,
+                [C.c_void_p, C.c_uint32, C.POINTER(C.c_char_p), C.POINTER(C.c_uint8), C.c_uint32, C.c_char_p,
+                 C.c_size_t, C.POINTER(C.c_size_t)],
             ),
         }
         for name, (res, args) in sig.items():
@@ -253,6 +265,12 @@ class Context:
             raise DeviceError(code, f"batch_finalize: {strerror(code)}")
         return code
 
+    def text(self, net: int, labels: "LabelTable") -> str:
+        """Canonical text of a finalized net, printed natively."""
+        names, arity, nl = labels.args()
+        return _print_call(lambda b, cap, n: self.lib.inet_batch_print(self.h, net, names, arity, nl, b, cap, n),
+                           "batch_print")
+
     def result(self, net: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         pa, pi, pe = _u32p(), _u32p(), _u32p()
         na, ni, ne = C.c_uint32(), C.c_uint32(), C.c_uint32()
@@ -284,6 +302,44 @@ def finalize_flat(agents: np.ndarray, iface: np.ndarray, eqs: np.ndarray, n_vars
     if code != OK:
         raise DeviceError(code, f"finalize_flat: {strerror(code)}")
     return agents, iface, eqs, alive[: len(eqs.reshape(-1)) // 2]
+
+
+class LabelTable:
+    """Label names and arities in the C layout the printer takes."""
+
+    def __init__(self, names, arities):
+        self._raw = [n.encode() for n in names]
+        self.names = (C.c_char_p * max(len(names), 1))(*self._raw)
+        self.arity = np.ascontiguousarray(arities, dtype=np.uint8)
+        self.n = len(names)
+
+    def args(self):
+        return self.names, self.arity.ctypes.data_as(C.POINTER(C.c_uint8)), self.n
+
+
+def _print_call(call, what: str) -> str:
+    n = C.c_size_t()
+    buf = C.create_string_buffer(1 << 16)
+    code = call(buf, len(buf), C.byref(n))
+    _check(code, what)
+    if n.value > len(buf):
+        buf = C.create_string_buffer(n.value)
+        code = call(buf, len(buf), C.byref(n))
+        _check(code, what)
+    return buf.raw[: n.value].decode()
+
+
+def print_flat(agents: np.ndarray, iface: np.ndarray, eqs: np.ndarray, labels: LabelTable) -> str:
+    """Canonical text (lang.print_configuration) of a flat normal form."""
+    lib = load_library()
+    agents = np.ascontiguousarray(agents, dtype=np.uint32).reshape(-1)
+    iface = np.ascontiguousarray(iface, dtype=np.uint32).reshape(-1)
+    eqs = np.ascontiguousarray(eqs, dtype=np.uint32).reshape(-1)
+    names, arity, nl = labels.args()
+    return _print_call(
+        lambda b, cap, n: lib.inet_print_flat(_ptr(agents), agents.size // 4, _ptr(iface), iface.size, _ptr(eqs),
+                                              eqs.size // 2, names, arity, nl, b, cap, n),
+        "print_flat")
 
 
 def jit_compile(blob: np.ndarray, tier: int = 1, threads: int = 1024) -> tuple[int, str]:

@@ -219,6 +219,8 @@ struct inet_ctx {
   int jit_style = -1;  // -1: per tier (measured defaults); env INET_B200_JITSTYLE overrides
   bool dev_final = true;  // tier S finalizes nets on the device; env INET_B200_DEVFINAL=0 disables
   std::vector<uint32_t> dev_rows;  // per net: device-finalized normal-form agents + 1 (0: host finalize)
+  uint32_t text_net = INET_NONE;   // inet_batch_print: the net whose text is cached
+  std::string text;
   bool exact_code = true;  // rule-set kernel variant with reference-loop (deferred equation) code
 };
 
@@ -819,6 +821,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     if (first == INET_OK && k.err) first = static_cast<int>(k.err);
   }
   c->reduced = true;
+  c->text_net = INET_NONE;
   c->results.assign(c->n_nets, inethost::NormalForm{});
   c->finalized.assign(c->n_nets, 0);
   if (fetch) {
@@ -1009,6 +1012,22 @@ int inet_batch_finalize(inet_ctx* c, uint32_t net, uint32_t n_threads) {
   if (!c) return INET_ERR_ARG;
   if (!c->reduced) return INET_ERR_STATE;
   return inethost::finalize_batch(*c, net, n_threads);
+}
+
+int inet_batch_print(inet_ctx* c, uint32_t net, const char* const* names, const uint8_t* arity, uint32_t n_labels,
+                     char* buf, size_t cap, size_t* len) {
+  if (!c || !len || (n_labels && (!names || !arity))) return INET_ERR_ARG;
+  if (!c->reduced || net >= c->n_nets || !c->finalized[net]) return INET_ERR_STATE;
+  if (c->text_net != net) {
+    const inethost::NormalForm& nf = c->results[net];
+    c->text_net = INET_NONE;
+    const int st = inethost::print_flat(nf.agents.data(), static_cast<uint32_t>(nf.agents.size() / 4), nf.iface.data(),
+                                        static_cast<uint32_t>(nf.iface.size()), nf.eqs.data(),
+                                        static_cast<uint32_t>(nf.eqs.size() / 2), names, arity, n_labels, c->text);
+    if (st) return st;
+    c->text_net = net;
+  }
+  return inethost::copy_text(c->text, buf, cap, len);
 }
 
 int inet_batch_result(inet_ctx* c, uint32_t net, const uint32_t** agents, uint32_t* n_agents, const uint32_t** iface,

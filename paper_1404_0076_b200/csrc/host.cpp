@@ -18,7 +18,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstring>
+#include <string>
 #include <thread>
+#include <unordered_map>
 
 namespace inethost {
 
@@ -300,10 +303,175 @@ int parallel_for(uint32_t n, uint32_t n_threads, const std::function<int(uint32_
   return first.load();
 }
 
+
+// ---------------------------------------------------------------------------
+// Canonical printer (restates lang.print_configuration, src/inet/lang.py:333-396,
+// with core.iter_vars order, core.py:96-104): equations oriented so that the
+// smaller structural skeleton (lang.py:347-360) is on the left, stably sorted
+// by (smaller, larger) skeleton, variables named x0, x1, ... in first-occurrence
+// preorder over the interface then the sorted equations, terms printed as
+// `Name` / `Name(c0,c1)`. Works on a flat normal form (preorder agents whose
+// refs index the same array), so large results print without building terms.
+namespace {
+
+struct Printer {
+  const uint32_t* ag;
+  uint32_t na;
+  const char* const* names;
+  const uint8_t* arity;
+  uint32_t nl;
+  uint64_t budget;  // agents a walk may visit (a tree visits each once)
+
+  bool agent_ok(uint32_t a) const { return a < na && ag[4 * a] < nl; }
+
+  // structural skeleton: Name( children ) with ? for variables
+  bool skeleton(uint32_t root, std::string& out) {
+    std::vector<uint32_t> st{root};
+    uint64_t seen = 0;
+    while (!st.empty()) {
+      const uint32_t t = st.back();
+      st.pop_back();
+      if (t == kNone - 1) {
+        out.push_back(')');
+        continue;
+      }
+      if (t == kNone) return false;
+      if (t & kVar) {
+        out.push_back('?');
+        continue;
+      }
+      if (!agent_ok(t) || ++seen > budget) return false;
+      const uint32_t lab = ag[4 * t];
+      out.append(names[lab]);
+      out.push_back('(');
+      st.push_back(kNone - 1);
+      for (int k = int(arity[lab]) - 1; k >= 0; --k) st.push_back(ag[4 * t + 1 + k]);
+    }
+    return true;
+  }
+
+  // first-occurrence variable numbering, preorder (children left to right)
+  bool assign(uint32_t root, std::unordered_map<uint32_t, uint32_t>& ids) {
+    std::vector<uint32_t> st{root};
+    uint64_t seen = 0;
+    while (!st.empty()) {
+      const uint32_t t = st.back();
+      st.pop_back();
+      if (t == kNone) return false;
+      if (t & kVar) {
+        ids.emplace(t & ~kVar, static_cast<uint32_t>(ids.size()));
+        continue;
+      }
+      if (!agent_ok(t) || ++seen > budget) return false;
+      const uint32_t lab = ag[4 * t];
+      for (int k = int(arity[lab]) - 1; k >= 0; --k) st.push_back(ag[4 * t + 1 + k]);
+    }
+    return true;
+  }
+
+  bool term(uint32_t root, const std::unordered_map<uint32_t, uint32_t>& ids, std::string& out) {
+    std::vector<uint32_t> st{root};
+    uint64_t seen = 0;
+    while (!st.empty()) {
+      const uint32_t t = st.back();
+      st.pop_back();
+      if (t == kNone - 1) {
+        out.push_back(')');
+        continue;
+      }
+      if (t == kNone - 2) {
+        out.push_back(',');
+        continue;
+      }
+      if (t & kVar) {
+        out.push_back('x');
+        out.append(std::to_string(ids.at(t & ~kVar)));
+        continue;
+      }
+      if (!agent_ok(t) || ++seen > budget) return false;
+      const uint32_t lab = ag[4 * t];
+      out.append(names[lab]);
+      const uint32_t n = arity[lab];
+      if (n == 0) continue;
+      out.push_back('(');
+      st.push_back(kNone - 1);
+      for (int k = int(n) - 1; k >= 0; --k) {
+        st.push_back(ag[4 * t + 1 + k]);
+        if (k) st.push_back(kNone - 2);
+      }
+    }
+    return true;
+  }
+};
+
+}  // namespace
+
+int print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface, uint32_t n_iface,
+               const uint32_t* eqs, uint32_t n_eqs, const char* const* names, const uint8_t* arity,
+               uint32_t n_labels, std::string& out) {
+  for (uint32_t l = 0; l < n_labels; ++l)
+    if (!names[l] || arity[l] > 3) return INET_ERR_ARG;
+  Printer p{agents, n_agents, names, arity, n_labels, uint64_t(n_agents) + 1};
+  // orientation and order of the equations
+  struct Eq {
+    uint32_t l, r;
+    std::string a, b;  // (smaller, larger) skeleton
+  };
+  std::vector<Eq> es(n_eqs);
+  for (uint32_t e = 0; e < n_eqs; ++e) {
+    std::string sl, sr;
+    if (!p.skeleton(eqs[2 * e], sl) || !p.skeleton(eqs[2 * e + 1], sr)) return INET_ERR_ARG;
+    if (sl <= sr)
+      es[e] = Eq{eqs[2 * e], eqs[2 * e + 1], std::move(sl), std::move(sr)};
+    else
+      es[e] = Eq{eqs[2 * e + 1], eqs[2 * e], std::move(sr), std::move(sl)};
+  }
+  std::stable_sort(es.begin(), es.end(), [](const Eq& x, const Eq& y) {
+    const int c = x.a.compare(y.a);
+    return c != 0 ? c < 0 : x.b < y.b;
+  });
+  std::unordered_map<uint32_t, uint32_t> ids;
+  for (uint32_t i = 0; i < n_iface; ++i)
+    if (!p.assign(iface[i], ids)) return INET_ERR_ARG;
+  for (const Eq& e : es)
+    if (!p.assign(e.l, ids) || !p.assign(e.r, ids)) return INET_ERR_ARG;
+  out.assign("net");
+  if (n_iface) out.push_back(' ');
+  for (uint32_t i = 0; i < n_iface; ++i) {
+    if (i) out.append(", ");
+    if (!p.term(iface[i], ids, out)) return INET_ERR_ARG;
+  }
+  out.append(" : ");
+  for (size_t k = 0; k < es.size(); ++k) {
+    if (k) out.append(", ");
+    if (!p.term(es[k].l, ids, out)) return INET_ERR_ARG;
+    out.append(" = ");
+    if (!p.term(es[k].r, ids, out)) return INET_ERR_ARG;
+  }
+  out.push_back(';');  // "net ... : ;" when no equation is left
+  return INET_OK;
+}
+
+int copy_text(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap) std::memcpy(buf, s.data(), std::min(cap, s.size()));
+  return INET_OK;
+}
 }  // namespace inethost
 
 extern "C" int inet_finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface,
                                   uint32_t* eqs, uint32_t n_eqs, uint32_t n_vars, uint8_t* alive) {
   if ((n_agents && !agents) || (n_iface && !iface) || (n_eqs && !eqs)) return INET_ERR_ARG;
   return inethost::finalize_flat(agents, n_agents, iface, n_iface, eqs, n_eqs, n_vars, alive);
+}
+
+extern "C" int inet_print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface, uint32_t n_iface,
+                               const uint32_t* eqs, uint32_t n_eqs, const char* const* names, const uint8_t* arity,
+                               uint32_t n_labels, char* buf, size_t cap, size_t* len) {
+  if ((n_agents && !agents) || (n_iface && !iface) || (n_eqs && !eqs) || (n_labels && (!names || !arity)) || !len)
+    return INET_ERR_ARG;
+  std::string text;
+  const int st = inethost::print_flat(agents, n_agents, iface, n_iface, eqs, n_eqs, names, arity, n_labels, text);
+  if (st) return st;
+  return inethost::copy_text(text, buf, cap, len);
 }

@@ -4,6 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <functional>
+#include <string>
 #include <vector>
 
 #include "../../include/inet_b200.h"
@@ -38,6 +39,12 @@ int validate_nets(const inet_ctx& c);
 // In-place finalize on mutable flat arrays; alive[e] = 1 for surviving equations.
 int finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface, uint32_t* eqs,
                   uint32_t n_eqs, uint32_t n_vars, uint8_t* alive);
+
+// Canonical text of a flat normal form (lang.print_configuration).
+int print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface, uint32_t n_iface,
+               const uint32_t* eqs, uint32_t n_eqs, const char* const* names, const uint8_t* arity,
+               uint32_t n_labels, std::string& out);
+int copy_text(const std::string& s, char* buf, size_t cap, size_t* len);
 
 // finalize + compaction of one fetched net.
 int finalize_net(const NetView& v, NormalForm& out);

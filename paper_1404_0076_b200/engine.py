@@ -253,6 +253,30 @@ class BatchResult:
     total_interactions: int
     total_communications: int
     max_rounds: int
+    texts: Optional[list] = None  # canonical text per net (as_text=True), printed natively
+
+
+def label_table(labels: Labels) -> _native.LabelTable:
+    """Names and arities of a label numbering, in the native printer's layout."""
+    tab = getattr(labels, "_table", None)
+    if tab is None or tab.n != len(labels.symbols):
+        tab = _native.LabelTable([s.name for s in labels.symbols], [s.arity for s in labels.symbols])
+        labels._table = tab
+    return tab
+
+
+def evaluate_text(config: Configuration, rules: RuleSet, cfg: Optional[EngineConfig] = None) -> tuple:
+    """Reduce ``config`` and return ``(text, total_interactions, total_communications)``.
+
+    ``text`` equals ``print_configuration(evaluate(config, rules, cfg).final)``
+    (lang.py:371-396) but is printed by the library from the flat normal form,
+    so large results (an 8,190-deep A(3,10) tower, L-system trees) never become
+    Python terms.
+    """
+    cfg = cfg if cfg is not None else EngineConfig(collect_stats=False)
+    out = evaluate_batch([config], rules, cfg, as_terms=False, as_text=True)
+    r = out.results[0]
+    return out.texts[0], r.total_interactions, r.total_communications
 
 
 def evaluate_batch(
@@ -261,8 +285,13 @@ def evaluate_batch(
     cfg: Optional[EngineConfig] = None,
     as_terms: bool = True,
     finalize_threads: int = 0,
+    as_text: bool = False,
 ) -> BatchResult:
-    """Reduce independent nets in one launch (one CTA per net)."""
+    """Reduce independent nets in one launch (one CTA per net).
+
+    ``as_text`` adds each normal form's canonical text (``print_configuration``
+    of the final configuration), printed natively from the flat normal form.
+    """
     cfg = cfg if cfg is not None else EngineConfig(collect_stats=False)
     if not configs:
         return BatchResult([], 0.0, 0, 0, 0)
@@ -284,10 +313,15 @@ def evaluate_batch(
         stats = [ctx.stats(i) for i in range(len(configs))]
         finals = [None] * len(configs)
         rows = [None] * len(configs)
-        if as_terms:
+        texts = None
+        if as_terms or as_text:
             ctx.finalize(0xFFFFFFFF, finalize_threads)
+        if as_terms:
             for i in range(len(configs)):
                 finals[i] = ctx.result(i)
+        if as_text:
+            tab = label_table(prep.labels)
+            texts = [ctx.text(i, tab) for i in range(len(configs))]
         if cfg.collect_stats:
             rows = [ctx.rounds(i) for i in range(len(configs))]
     out = []
@@ -301,7 +335,7 @@ def evaluate_batch(
         if rows[i] is not None:
             loops = [LS(j + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for j, r in enumerate(rows[i])]
         out.append(ER(final, loops, int(stats[i].interactions), int(stats[i].communications)))
-    return BatchResult(out, ms, ti, tc, mr)
+    return BatchResult(out, ms, ti, tc, mr, texts)
 
 
 def evaluate_sharded(

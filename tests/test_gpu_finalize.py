@@ -98,3 +98,27 @@ def test_interface_variables_fall_back_to_host():
     pair = Configuration((Var(0),), (Equation(Var(0), Agent(syms["Z"])),))
     nets = [wire, closed, pair, wire, closed]
     _compare(nets, prog.rules)
+
+
+def test_native_text_equals_python_printer():
+    from paper_1404_0076_b200 import evaluate, evaluate_batch, evaluate_text
+
+    prog = programs.program("ackermann")
+    rng = random.Random(11)
+    nets = [prog.build_input(rng.randint(0, 3), rng.randint(0, 5)) for _ in range(100)]
+    out = evaluate_batch(nets, prog.rules, EngineConfig(collect_stats=False), as_text=True)
+    for res, text in zip(out.results, out.texts):
+        assert text == print_configuration(res.final)
+    rules = programs.load_rules("arith")
+    arith = [_random_arith_net(rng, rules.symbols, rng.choice([8, 40, 200])) for _ in range(100)]
+    out = evaluate_batch(arith, rules, EngineConfig(collect_stats=False), as_text=True)
+    for res, text in zip(out.results, out.texts):
+        assert text == print_configuration(res.final)
+    # single nets (tiers M / C / X, host finalize): the big normal forms
+    for name, params in (("ackermann", (3, 8)), ("lsystem", (22,)), ("fibonacci", (12,))):
+        p = programs.program(name)
+        cfg = p.build_input(*params)
+        text, ints, _ = evaluate_text(cfg, p.rules)
+        res = evaluate(cfg, p.rules, EngineConfig(collect_stats=False))
+        assert ints == res.total_interactions
+        assert text == print_configuration(res.final), name
