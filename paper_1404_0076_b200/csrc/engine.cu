@@ -458,10 +458,11 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
     return 1024;
   }
   // measured on 4096/1024/512/256 x A(3,6): 128 threads once there are about
-  // as many nets as SMs x 7, 256 below that
+  // as many nets as SMs x 7, 256 below that; a few nets (one per SM) are
+  // round-latency bound: 256 threads (fib(18): 2.72 ms vs 3.21 ms at 1024)
   if (c->n_nets >= 1024) return 128;
   if (c->n_nets >= 256) return 256;
-  return c->n_nets >= 16 ? 512 : 1024;
+  return c->n_nets >= 16 ? 512 : 256;
 }
 
 // CTA size of tier C (one CTA per SM of the cluster).
@@ -1021,7 +1022,7 @@ int inet_batch_print(inet_ctx* c, uint32_t net, const char* const* names, const 
   if (c->text_net != net) {
     const inethost::NormalForm& nf = c->results[net];
     c->text_net = INET_NONE;
-    const int st = inethost::print_flat(nf.agents.data(), static_cast<uint32_t>(nf.agents.size() / 4), nf.iface.data(),
+    const int st = inethost::print_flat(nf.agent_data(), nf.n_agents(), nf.iface.data(),
                                         static_cast<uint32_t>(nf.iface.size()), nf.eqs.data(),
                                         static_cast<uint32_t>(nf.eqs.size() / 2), names, arity, n_labels, c->text);
     if (st) return st;
@@ -1035,8 +1036,8 @@ int inet_batch_result(inet_ctx* c, uint32_t net, const uint32_t** agents, uint32
   if (!c) return INET_ERR_ARG;
   if (!c->reduced || net >= c->n_nets || !c->finalized[net]) return INET_ERR_STATE;
   const inethost::NormalForm& nf = c->results[net];
-  if (agents) *agents = nf.agents.data();
-  if (n_agents) *n_agents = static_cast<uint32_t>(nf.agents.size() / 4);
+  if (agents) *agents = nf.agent_data();
+  if (n_agents) *n_agents = nf.n_agents();
   if (iface) *iface = nf.iface.data();
   if (n_iface) *n_iface = static_cast<uint32_t>(nf.iface.size());
   if (eqs) *eqs = nf.eqs.data();
@@ -1085,7 +1086,9 @@ int finalize_batch(inet_ctx& c, uint32_t net, uint32_t n_threads) {
       const uint32_t* ag = c.h_agents.data() + size_t(i) * c.agent_pitch * 4;
       const uint32_t* rs = c.h_resid.data() + size_t(i) * c.resid_pitch * 2;
       const uint32_t ni = static_cast<uint32_t>(c.iface_off[i + 1] - c.iface_off[i]);
-      nf.agents.assign(ag, ag + size_t(rows - 1) * 4);
+      nf.agents.clear();
+      nf.ext_agents = ag;
+      nf.ext_n = rows - 1;
       nf.iface.resize(ni);
       for (uint32_t k = 0; k < ni; ++k) nf.iface[k] = rs[2 * k];
       nf.eqs.clear();

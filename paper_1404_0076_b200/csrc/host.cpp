@@ -221,6 +221,8 @@ int finalize_net(const NetView& v, NormalForm& out) {
   std::vector<uint32_t>& ag = sc.ag;
   std::vector<uint32_t>& ifc = sc.ifc;
   std::vector<uint32_t>& eq = sc.eq;
+  out.ext_agents = nullptr;
+  out.ext_n = 0;
   ag.assign(v.agents, v.agents + size_t(v.n_agents) * 4);
   ifc.assign(v.iface, v.iface + v.n_iface);
   eq.assign(v.residual, v.residual + size_t(v.n_residual) * 2);

@@ -20,6 +20,12 @@ struct NormalForm {
   std::vector<uint32_t> agents;
   std::vector<uint32_t> iface;
   std::vector<uint32_t> eqs;
+  // finalized on the device: the agent records stay in the context's
+  // page-locked result buffer (valid until the next reduction)
+  const uint32_t* ext_agents = nullptr;
+  uint32_t ext_n = 0;
+  const uint32_t* agent_data() const { return ext_agents ? ext_agents : agents.data(); }
+  uint32_t n_agents() const { return ext_agents ? ext_n : static_cast<uint32_t>(agents.size() / 4); }
 };
 
 // Read-only view of one reduced net as fetched from the device.
