@@ -1232,10 +1232,12 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
 #endif
   const uint32_t lane = threadIdx.x & 31u;
   c.cap_def = d.cap_def;
-  // Per-round totals are only needed for the per-round rows and tier M's
-  // hand-over threshold; otherwise each thread keeps its own running totals,
-  // summed once after the loop.
-  const bool per_round = d.stats != nullptr || (kTier == kTierM && sh.promote_ints != 0);
+  // Per-round totals are only needed for the per-round rows; otherwise each
+  // thread keeps its own running totals, summed once after the loop. (Tier
+  // M's hand-over threshold counts queued pairs instead: the pairs queued in
+  // round r are exactly the interactions of round r + 1.)
+  const bool per_round = d.stats != nullptr;
+  unsigned long long tot_q = 0;
   c.ints = c.comms = 0;
   c.parked = 0;
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, nd = 0, rounds = 1;
@@ -1382,7 +1384,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
       stop = true;
       stop_err = INET_ERR_LOOP_CAP;
-    } else if (kTier == kTierM && sh.promote_ints && tot_i >= sh.promote_ints) {
+    } else if (kTier == kTierM && sh.promote_ints && (tot_q += q) >= sh.promote_ints) {
       stop = true;  // a large net: the host hands it over to a cluster
       stop_err = kPromote;
     }
