@@ -1638,6 +1638,11 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   uint32_t N = d.n_in_eqs, excl = 0, rounds = 1, stop_err = 0;
   bool stop = false, mail_any = false;
   const bool writer = rank == 0 && threadIdx.x == 0;
+  // per-round totals only for the per-round rows; otherwise per-thread
+  // running totals, summed once after the loop
+  const bool per_round = d.stats != nullptr;
+  c.ints = c.comms = 0;
+  c.parked = 0;
   if (!fits) {
     stop = true;
     stop_err = INET_ERR_ARENA;
@@ -1655,8 +1660,10 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     c.hi_a = hi_a;
     c.lo_v = lo_v;
     c.hi_v = hi_v;
-    c.ints = c.comms = 0;
-    c.parked = 0;
+    if (per_round) {
+      c.ints = c.comms = 0;
+      c.parked = 0;
+    }
     c.inq = lqueue + (r & 1u) * 16 * cap_q;
     c.dout = sh.exact ? d.deferred + ((r & 1u) * G + rank) * c.cap_def : nullptr;
     c.outc = outc3 + (r % 3) * 32;
@@ -1768,7 +1775,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
       }
     }
     CT_MARK(1);
-    {
+    if (per_round) {
       const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
       const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
       const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
@@ -1864,6 +1871,16 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     for (int i = 0; i < 4; ++i)
       atomicAdd(reinterpret_cast<unsigned long long*>(d.rule_hist) + 32 + i, ct_sum[i]);
 #endif
+  if (!per_round) {  // this CTA's totals (ctl->tot_* are unused by the loop of this tier)
+    const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
+    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
+    const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
+    if (lane == 0) {
+      if (wi) atomicAdd(&ctl->tot_i, static_cast<unsigned long long>(wi));
+      if (wc) atomicAdd(&ctl->tot_c, static_cast<unsigned long long>(wc));
+      if (wp) atomicAdd(&ctl->parked_total, wp);
+    }
+  }
   // ---- results. High-water marks of the interleaved id spaces.
   uint32_t a_hw = d.n_in_agents, v_hw = d.n_in_vars;
   uint32_t e_code = 0, e_a = 0, e_b = 0;
@@ -1924,6 +1941,15 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
       const uint32_t tot = block_scan_flag(v != kNone, ctl->scratch, &off);
       if (v != kNone && base + off < d.cap_vars) d.residual[base + off] = make_uint2(kVar | x, v);
       base += tot;
+    }
+  }
+  if (writer && !per_round) {
+    for (uint32_t k = 0; k < G; ++k) {
+      const uint32_t* ti = reinterpret_cast<const uint32_t*>(&ctl->tot_i);
+      const uint32_t* tc = reinterpret_cast<const uint32_t*>(&ctl->tot_c);
+      tot_i += dsmem_ld(ti, k) | (static_cast<unsigned long long>(dsmem_ld(ti + 1, k)) << 32);
+      tot_c += dsmem_ld(tc, k) | (static_cast<unsigned long long>(dsmem_ld(tc + 1, k)) << 32);
+      parked_tot += static_cast<int32_t>(dsmem_ld(&ctl->parked_total, k));
     }
   }
   if (writer) {
