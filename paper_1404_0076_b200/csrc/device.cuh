@@ -447,16 +447,55 @@ __device__ __forceinline__ uint4 unpack_agent(const uint2& w) {
   return make_uint4(w.x & 0xFFFFu, ref32(w.x >> 16), ref32(w.y & 0xFFFFu), ref32(w.y >> 16));
 }
 
+// Tier S keeps references inside the kernel in a sign-extended form: variable
+// x is 0xFFFF8000 | x (bit 31 still marks a variable, kNone is still all ones,
+// agents are plain indices), so the 16-bit halves of the 8-byte agent records
+// convert with one sign extension and one mask instead of ref16/ref32. Every
+// other tier uses the standard form (INET_VAR_BIT | x). Conversions happen only
+// where tier S meets global memory: the input, the residual equations and the
+// arena / normal-form copies.
+template <int kTier>
+__device__ __forceinline__ constexpr uint32_t vtag() {
+  return kTier == kTierS ? 0xFFFF8000u : kVar;
+}
+template <int kTier>
+__device__ __forceinline__ uint32_t ref_in(uint32_t r) {  // standard -> internal
+  if constexpr (kTier == kTierS) return (r != kNone && (r & kVar)) ? (r | 0xFFFF8000u) : r;
+  else return r;
+}
+template <int kTier>
+__device__ __forceinline__ uint32_t ref_out(uint32_t r) {  // internal -> standard
+  if constexpr (kTier == kTierS) return (r != kNone && (r & kVar)) ? (kVar | (r & 0x7FFFu)) : r;
+  else return r;
+}
+template <int kTier>
+__device__ __forceinline__ uint4 agent_in(const uint4& v) {
+  return make_uint4(v.x, ref_in<kTier>(v.y), ref_in<kTier>(v.z), ref_in<kTier>(v.w));
+}
+template <int kTier>
+__device__ __forceinline__ uint4 agent_out(const uint4& v) {
+  return make_uint4(v.x, ref_out<kTier>(v.y), ref_out<kTier>(v.z), ref_out<kTier>(v.w));
+}
+__device__ __forceinline__ uint32_t sext16(uint32_t h) {  // low 16 bits, sign-extended
+  return static_cast<uint32_t>(static_cast<int32_t>(h << 16) >> 16);
+}
+__device__ __forceinline__ uint2 pack_agent_s(const uint4& v) {
+  return make_uint2(__byte_perm(v.x, v.y, 0x5410), __byte_perm(v.z, v.w, 0x5410));
+}
+__device__ __forceinline__ uint4 unpack_agent_s(const uint2& w) {
+  return make_uint4(w.x & 0xFFFFu, sext16(w.x >> 16), sext16(w.y), sext16(w.y >> 16));
+}
+
 template <int kTier>
 __device__ __forceinline__ uint4 ld_agent(const Round<kTier>& c, uint32_t a) {
   if constexpr (kTier == kTierC) return dsmem_ld4(c.agents + (a >> c.gshift), a & (c.stride - 1));
-  else if constexpr (Traits<kTier>::kCompact) return unpack_agent(reinterpret_cast<const uint2*>(c.agents)[a]);
+  else if constexpr (Traits<kTier>::kCompact) return unpack_agent_s(reinterpret_cast<const uint2*>(c.agents)[a]);
   else return c.agents[a];
 }
 template <int kTier>
 __device__ __forceinline__ void st_agent(const Round<kTier>& c, uint32_t a, const uint4& v) {
   if constexpr (kTier == kTierC) dsmem_st4(c.agents + (a >> c.gshift), a & (c.stride - 1), v);
-  else if constexpr (Traits<kTier>::kCompact) reinterpret_cast<uint2*>(c.agents)[a] = pack_agent(v);
+  else if constexpr (Traits<kTier>::kCompact) reinterpret_cast<uint2*>(c.agents)[a] = pack_agent_s(v);
   else c.agents[a] = v;
 }
 template <int kTier>
@@ -647,7 +686,7 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
 #endif
     uint32_t key;
     key_of(l, r, key, val);
-    x = key & ~kVar;
+    x = key & ~vtag<kTier>();
     old = exch_slot(c, x, val);
   }
 }
@@ -660,7 +699,7 @@ __device__ __forceinline__ void link(Round<kTier>& c, uint32_t l, uint32_t r) {
   }
   uint32_t key, val;
   key_of(l, r, key, val);
-  const uint32_t x = key & ~kVar;
+  const uint32_t x = key & ~vtag<kTier>();
   settle(c, x, exch_slot(c, x, val), val);
 }
 
@@ -673,7 +712,7 @@ __device__ __forceinline__ bool jit_alloc_vars(Round<kTier>& c, uint32_t (&f)[N]
   if (!alloc_vars(c, N, k)) return false;
 #pragma unroll
   for (uint32_t j = 0; j < N; ++j)
-    f[j] = kVar | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
+    f[j] = vtag<kTier>() | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
   return true;
 }
 
@@ -695,7 +734,7 @@ __device__ __forceinline__ bool jit_alloc_vars_n(Round<kTier>& c, uint32_t n, ui
 #pragma unroll
   for (uint32_t j = 0; j < N; ++j)
     if (j < n)
-      f[j] = kVar | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
+      f[j] = vtag<kTier>() | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
   return true;
 }
 
@@ -757,7 +796,7 @@ __device__ __forceinline__ bool jit_warp_alloc(Round<kTier>& c, uint32_t nf, uin
   for (uint32_t j = 0; j < MF; ++j)
     if (j < nf) {
       const uint32_t q = tv + ex_f + j;
-      f[j] = kVar | (q < av_v ? static_cast<uint32_t>(c.vring[(c.lo_v + q) & c.vmask]) : bump_var(c, bv + (q - fb_v)));
+      f[j] = vtag<kTier>() | (q < av_v ? static_cast<uint32_t>(c.vring[(c.lo_v + q) & c.vmask]) : bump_var(c, bv + (q - fb_v)));
     }
 #pragma unroll
   for (uint32_t j = 0; j < MX; ++j)
@@ -808,7 +847,7 @@ __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uin
 #pragma unroll
   for (uint32_t j = 0; j < MX; ++j) ra[j] = c.aring[(c.lo_a + ta + j) & c.amask];
 #pragma unroll
-  for (uint32_t j = 0; j < MF; ++j) f[j] = kVar | (j < gv ? rv[j] : bump_var(c, bv + (j - gv)));
+  for (uint32_t j = 0; j < MF; ++j) f[j] = vtag<kTier>() | (j < gv ? rv[j] : bump_var(c, bv + (j - gv)));
 #pragma unroll
   for (uint32_t j = 0; j < MX; ++j) g[j] = j < ga ? ra[j] : bump_agent(c, ba + (j - ga));
   return true;
@@ -823,7 +862,7 @@ __device__ __forceinline__ bool jit_prep(Round<kTier>& c, uint32_t l, uint32_t r
   }
   uint32_t key;
   key_of(l, r, key, val);
-  x = key & ~kVar;
+  x = key & ~vtag<kTier>();
   return true;
 }
 
@@ -869,7 +908,7 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
   INET_TMARK(c, 2);
   INET_TR(c, 3);
   auto fresh = [&](uint32_t j) -> uint32_t {
-    return kVar | (j < fv.got ? static_cast<uint32_t>(c.vring[(fv.pos + j) & c.vmask]) : bump_var(c, fv.bump + (j - fv.got)));
+    return vtag<kTier>() | (j < fv.got ? static_cast<uint32_t>(c.vring[(fv.pos + j) & c.vmask]) : bump_var(c, fv.bump + (j - fv.got)));
   };
   auto extra = [&](uint32_t q) -> uint32_t {
     return q < na.got ? static_cast<uint32_t>(c.aring[(na.pos + q) & c.amask]) : bump_agent(c, na.bump + (q - na.got));
@@ -946,7 +985,7 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
       } else {
         uint32_t key;
         key_of(el, er, key, vals[e]);
-        xs[e] = key & ~kVar;
+        xs[e] = key & ~vtag<kTier>();
         olds[e] = exch_slot(c, xs[e], vals[e]);
       }
     }
@@ -1090,7 +1129,7 @@ __device__ uint32_t finalize_smem(const Round<kTier>& c, const NetDesc& d, Ctl* 
     // a consumed slot keeps its value, marked (a variable is met at most once)
     auto resolve = [&](uint32_t t) {
       for (uint32_t guard = 0; t != kNone && (t & kVar) && guard <= n_parked; ++guard) {
-        const uint32_t x = t & ~kVar;
+        const uint32_t x = t & ~vtag<kTier>();
         const uint32_t v = x < hw ? c.vslot[x] : kNone;
         if (v == kNone) break;
         if (v & kConsumed) {
@@ -1104,7 +1143,7 @@ __device__ uint32_t finalize_smem(const Round<kTier>& c, const NetDesc& d, Ctl* 
       return t;
     };
     for (uint32_t i = 0; i < ni && ok; ++i) {
-      const uint32_t root = resolve(d.in_iface[i]);
+      const uint32_t root = resolve(ref_in<kTier>(d.in_iface[i]));
       ifc[i] = root;
       if (root == kNone || (root & kVar)) continue;
       stack[sp++] = root;
@@ -1136,12 +1175,12 @@ __device__ uint32_t finalize_smem(const Round<kTier>& c, const NetDesc& d, Ctl* 
   // arena as the host finalize expects it): ports are resolved again here
   auto map = [&](uint32_t t) {
     for (uint32_t guard = 0; t != kNone && (t & kVar) && guard <= n_parked; ++guard) {
-      const uint32_t x = t & ~kVar;
+      const uint32_t x = t & ~vtag<kTier>();
       const uint32_t v = x < hw ? c.vslot[x] : kNone;
       if (v == kNone) break;
       t = v & ~kConsumed;
     }
-    return (t == kNone || (t & kVar)) ? t : static_cast<uint32_t>(remap[t]);
+    return (t == kNone || (t & kVar)) ? ref_out<kTier>(t) : static_cast<uint32_t>(remap[t]);
   };
   for (uint32_t j = threadIdx.x; j < rows - 1; j += blockDim.x) {
     const uint4 A = ld_agent(c, order[j]);
@@ -1197,7 +1236,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   const bool fits = d.n_in_agents <= c.cap_agents && d.n_in_vars <= c.cap_vars;
   for (uint32_t i = threadIdx.x; i < c.cap_vars; i += blockDim.x) c.vslot[i] = kNone;
   if (fits)
-    for (uint32_t i = threadIdx.x; i < d.n_in_agents; i += blockDim.x) st_agent(c, i, d.in_agents[i]);
+    for (uint32_t i = threadIdx.x; i < d.n_in_agents; i += blockDim.x) st_agent(c, i, agent_in<kTier>(d.in_agents[i]));
   {
     uint32_t* w = reinterpret_cast<uint32_t*>(ctl);
     for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += blockDim.x) w[i] = 0;
@@ -1276,14 +1315,14 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
         for (uint32_t b = threadIdx.x & ~31u; b < n; b += blockDim.x) {
           const uint32_t i = b + lane;
           const bool v = i < n && !c.failed;
-          const uint2 eq = v ? d.in_eqs[i] : make_uint2(0, 0);
+          const uint2 eq = v ? make_uint2(ref_in<kTier>(d.in_eqs[i].x), ref_in<kTier>(d.in_eqs[i].y)) : make_uint2(0, 0);
           const bool act = v && ((eq.x | eq.y) & kVar) == 0;
           interact_w(c, act, eq.x, eq.y);
           if (v && !act && !c.failed) link(c, eq.x, eq.y);
         }
       } else {
         for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
-          const uint2 eq = d.in_eqs[i];
+          const uint2 eq = make_uint2(ref_in<kTier>(d.in_eqs[i].x), ref_in<kTier>(d.in_eqs[i].y));
           if (((eq.x | eq.y) & kVar) == 0)
             interact(c, eq.x, eq.y);
           else
@@ -1439,7 +1478,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     const uint32_t v = x < hw ? c.vslot[x] : kNone;
     uint32_t off;
     const uint32_t tot = block_scan_flag(v != kNone, ctl->scratch, &off);
-    if (v != kNone && base + off < d.cap_vars) d.residual[base + off] = make_uint2(kVar | x, v);
+    if (v != kNone && base + off < d.cap_vars) d.residual[base + off] = make_uint2(kVar | x, ref_out<kTier>(v));
     base += tot;
   }
   const uint32_t ahw = min(ctl->agent_bump, c.cap_agents);
@@ -1449,7 +1488,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   }
   if constexpr (T::kAgentsSmem) {
     const uint32_t n_copy = nf_rows ? 0u : min(ahw, d.cap_agents);
-    for (uint32_t i = threadIdx.x; i < n_copy; i += blockDim.x) d.agents[i] = ld_agent(c, i);
+    for (uint32_t i = threadIdx.x; i < n_copy; i += blockDim.x) d.agents[i] = agent_out<kTier>(ld_agent(c, i));
   }
   if (threadIdx.x == 0) {
     NetCtl* g = d.ctl;
