@@ -1282,8 +1282,9 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, nd = 0, rounds = 1;
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
+  uint32_t set = 1, set_next = 2;  // r % 3 and (r + 1) % 3, rotated
   for (uint32_t r = 1; !stop; ++r) {
-    RoundCtr* cur = &ctl->ctr3[r % 3];
+    RoundCtr* cur = &ctl->ctr3[set];
     c.cur = cur;
     c.lo_a = lo_a;
     c.hi_a = hi_a;
@@ -1293,7 +1294,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       c.ints = c.comms = 0;
       c.parked = 0;
     }
-    if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(&ctl->ctr3[(r + 1) % 3])[threadIdx.x] = 0;
+    if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(&ctl->ctr3[set_next])[threadIdx.x] = 0;
     c.dout = sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
     c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + (r & 1u) * qstride)
                        : static_cast<void*>(static_cast<uint2*>(q0) + (r & 1u) * qstride);
@@ -1393,9 +1394,13 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     hi_a += wa;
     lo_v += min(k.vtake, hi_v - lo_v);
     hi_v += wv;
-    parked_tot += k.parked;
-    tot_i += k.ints;
-    tot_c += k.comms;
+    if (per_round) {
+      parked_tot += k.parked;
+      tot_i += k.ints;
+      tot_c += k.comms;
+    }
+    set = set_next;
+    set_next = set_next == 2 ? 0u : set_next + 1;
     if (threadIdx.x == 0 && d.stats) {
 #ifdef INET_NO_TIMER
       const unsigned long long now = 0;
