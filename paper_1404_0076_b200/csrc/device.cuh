@@ -2111,6 +2111,11 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
   uint2* const Q = d.queue;
+  // per-round totals only for the per-round rows (every block's atomics on
+  // three global counters each round otherwise)
+  const bool per_round = d.stats != nullptr;
+  c.ints = c.comms = 0;
+  c.parked = 0;
   for (uint32_t r = 1; !stop; ++r) {
     RoundCtr* cur = &g->ctr3[r % 3];
     c.cur = cur;
@@ -2118,8 +2123,10 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
     c.hi_a = hi_a;
     c.lo_v = lo_v;
     c.hi_v = hi_v;
-    c.ints = c.comms = 0;
-    c.parked = 0;
+    if (per_round) {
+      c.ints = c.comms = 0;
+      c.parked = 0;
+    }
     c.dout = nullptr;
     c.out = Q + (r & 1u) * c.cap_queue;
     if (blockIdx.x == 0 && threadIdx.x < sizeof(RoundCtr) / 4)
@@ -2143,7 +2150,7 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
         interact_w(c, v, e.x, e.y);
       }
     }
-    {
+    if (per_round) {
       const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
       const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
       const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
@@ -2200,7 +2207,22 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
     }
   }
   if (lead && stop_err) atomicCAS(&ctl->err_code, 0u, stop_err);
+  if (!per_round) {  // the run's totals, once
+    const uint32_t wi = __reduce_add_sync(0xFFFFFFFFu, c.ints);
+    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c.comms);
+    const int32_t wp = __reduce_add_sync(0xFFFFFFFFu, c.parked);
+    if (lane == 0) {
+      if (wi) atomicAdd(&ctl->tot_i, static_cast<unsigned long long>(wi));
+      if (wc) atomicAdd(&ctl->tot_c, static_cast<unsigned long long>(wc));
+      if (wp) atomicAdd(&ctl->parked_total, wp);
+    }
+  }
   grid_barrier(g);
+  if (!per_round) {  // (L2 reads: the atomics bypassed this SM's L1)
+    tot_i = __ldcg(&ctl->tot_i);
+    tot_c = __ldcg(&ctl->tot_c);
+    parked_tot = __ldcg(&ctl->parked_total);
+  }
   // ---- results: residual parked equations in variable-id order (two passes)
   const uint32_t v_hw = min(ctl->var_bump, c.cap_vars), a_hw = min(ctl->agent_bump, c.cap_agents);
   const uint32_t per = (v_hw + gridDim.x - 1) / gridDim.x;
