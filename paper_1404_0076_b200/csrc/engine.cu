@@ -657,6 +657,9 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     fetch_ctl();
     c->tier = tier;
     c->shape = sh;
+    if (std::getenv("INET_B200_DEBUG"))
+      std::fprintf(stderr, "inet_b200: attempt tier %d caps %u/%u/%u: %.3f ms, net 0 status 0x%x\n", tier, ca, cv, cq, ms,
+                   c->ctl[0].err);
     return INET_OK;
   };
   if (!user_caps && c->n_nets > 1 && c->max_in_agents <= 512 && c->max_in_vars <= 512) {

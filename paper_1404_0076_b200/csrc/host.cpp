@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -210,6 +211,88 @@ int finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t
   return INET_OK;
 }
 
+namespace {
+
+// Fast path of finalize_net (the host twin of the device's finalize_smem):
+// walk the net from the interface in preorder, replacing every variable whose
+// parked equation is known by that equation's other side at the variable's
+// other occurrence — where the reference's elimination writes it. When the
+// walk consumes every parked equation and meets no agent twice, the result is
+// the one the general pass produces (tests/test_gpu_finalize.py compares the
+// two); otherwise return false and the general pass runs.
+bool finalize_walk(const NetView& v, NormalForm& out, std::vector<uint32_t>& val, std::vector<uint32_t>& remap,
+                   std::vector<uint32_t>& order, std::vector<uint32_t>& stack, std::vector<uint32_t>& ports) {
+  constexpr uint32_t kUsed = 0xFFFFFFFEu;  // a parked equation already applied
+  val.assign(v.n_vars, kNone);
+  for (uint32_t e = 0; e < v.n_residual; ++e) {
+    const uint32_t x = v.residual[2 * e], t = v.residual[2 * e + 1];
+    if (!is_var(x) || (x & ~kVar) >= v.n_vars || t == kUsed || val[x & ~kVar] != kNone) return false;
+    val[x & ~kVar] = t;
+  }
+  uint32_t consumed = 0;
+  bool ok = true;
+  auto resolve = [&](uint32_t t) {
+    for (uint32_t guard = 0; is_var(t) && guard <= v.n_residual; ++guard) {
+      const uint32_t x = t & ~kVar;
+      if (x >= v.n_vars) {
+        ok = false;
+        break;
+      }
+      const uint32_t w = val[x];
+      if (w == kNone) break;
+      if (w == kUsed) {
+        ok = false;
+        break;
+      }
+      val[x] = kUsed;
+      consumed += 1;
+      t = w;
+    }
+    return t;
+  };
+  remap.assign(v.n_agents, kNone);
+  order.clear();
+  ports.clear();
+  out.iface.resize(v.n_iface);
+  for (uint32_t i = 0; i < v.n_iface && ok; ++i) {
+    const uint32_t root = resolve(v.iface[i]);
+    out.iface[i] = root;
+    if (root == kNone || is_var(root)) continue;
+    stack.clear();
+    stack.push_back(root);
+    while (!stack.empty() && ok) {
+      const uint32_t a = stack.back();
+      stack.pop_back();
+      if (a >= v.n_agents || remap[a] != kNone) {
+        ok = false;
+        break;
+      }
+      remap[a] = static_cast<uint32_t>(order.size());
+      order.push_back(a);
+      const uint32_t* rec = v.agents + 4 * size_t(a);
+      const uint32_t p0 = resolve(rec[1]), p1 = resolve(rec[2]), p2 = resolve(rec[3]);
+      ports.push_back(p0);
+      ports.push_back(p1);
+      ports.push_back(p2);
+      if (p2 != kNone && !is_var(p2)) stack.push_back(p2);
+      if (p1 != kNone && !is_var(p1)) stack.push_back(p1);
+      if (p0 != kNone && !is_var(p0)) stack.push_back(p0);
+    }
+  }
+  if (!ok || consumed != v.n_residual) return false;
+  auto map_ref = [&](uint32_t t) { return (t == kNone || is_var(t)) ? t : remap[t]; };
+  out.agents.resize(order.size() * 4);
+  for (size_t j = 0; j < order.size(); ++j) {
+    out.agents[4 * j] = v.agents[4 * size_t(order[j])];
+    for (int k = 0; k < 3; ++k) out.agents[4 * j + 1 + k] = map_ref(ports[3 * j + k]);
+  }
+  for (uint32_t i = 0; i < v.n_iface; ++i) out.iface[i] = map_ref(out.iface[i]);
+  out.eqs.clear();
+  return true;
+}
+
+}  // namespace
+
 int finalize_net(const NetView& v, NormalForm& out) {
   // per-thread scratch, reused across the nets a worker finalizes (a batch of
   // 4096 nets would otherwise spend most of its time in the allocator)
@@ -218,6 +301,12 @@ int finalize_net(const NetView& v, NormalForm& out) {
     Finalizer f{};
   };
   thread_local Scratch sc;
+  out.ext_agents = nullptr;
+  out.ext_n = 0;
+  // (INET_B200_HOSTWALK=0 forces the general pass: the tests compare the two)
+  const char* walk_env = std::getenv("INET_B200_HOSTWALK");
+  if ((!walk_env || std::atoi(walk_env) != 0) && finalize_walk(v, out, sc.remap, sc.order, sc.stack, sc.eq, sc.ifc))
+    return INET_OK;
   std::vector<uint32_t>& ag = sc.ag;
   std::vector<uint32_t>& ifc = sc.ifc;
   std::vector<uint32_t>& eq = sc.eq;

@@ -48,10 +48,19 @@ def _compare(nets, rules, orules=None, want_device=None):
     host = _ctx(False)
     try:
         prep, got = _reduce(dev, nets, rules)
-        _, ref = _reduce(host, nets, rules)
+        # the reference side: host finalize by the general elimination pass
+        # (not the host's own preorder-walk fast path)
+        os.environ["INET_B200_HOSTWALK"] = "0"
+        try:
+            _, ref = _reduce(host, nets, rules)
+        finally:
+            del os.environ["INET_B200_HOSTWALK"]
+        _, walk = _reduce(host, nets, rules)  # host fast path
     finally:
         dev.close()
         host.close()
+    for (_, aw, iw, ew), (_, ah, ih, eh) in zip(walk, ref):
+        assert np.array_equal(aw, ah) and np.array_equal(iw, ih) and np.array_equal(ew, eh)
     n_dev = 0
     for i, ((sd, ad, idf, ed), (sh, ah, ih, eh)) in enumerate(zip(got, ref)):
         assert sd.tier == 0, "these batches must run in tier S"
@@ -122,3 +131,21 @@ def test_native_text_equals_python_printer():
         res = evaluate(cfg, p.rules, EngineConfig(collect_stats=False))
         assert ints == res.total_interactions
         assert text == print_configuration(res.final), name
+
+
+@pytest.mark.parametrize("name,params", [("lsystem", (20,)), ("ackermann", (3, 7)), ("fibonacci", (14,))])
+def test_host_walk_equals_general_finalize_on_single_nets(name, params):
+    prog = programs.program(name)
+    nets = [prog.build_input(*params)]
+    ctx = _ctx(True)
+    try:
+        os.environ["INET_B200_HOSTWALK"] = "0"
+        try:
+            _, ref = _reduce(ctx, nets, prog.rules)
+        finally:
+            del os.environ["INET_B200_HOSTWALK"]
+        _, walk = _reduce(ctx, nets, prog.rules)
+    finally:
+        ctx.close()
+    (_, aw, iw, ew), (_, ah, ih, eh) = walk[0], ref[0]
+    assert np.array_equal(aw, ah) and np.array_equal(iw, ih) and np.array_equal(ew, eh)
