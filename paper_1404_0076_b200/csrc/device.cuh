@@ -432,25 +432,12 @@ __device__ __forceinline__ uint32_t dsmem_exch(const void* p, uint32_t rank, uin
 }
 
 // Tier S keeps agents as 8 bytes {label, p0 | p1, p2} with 16-bit refs
-// (bit 15 = variable, 0xFFFF = none; its arenas hold < 32768 ids), which
-// fits more nets per SM.
-// Branch-free: kNone maps to 0xFFFF and back because variable 0x7FFF never
-// exists in these arenas (< 32768 ids, the top one unused).
-__device__ __forceinline__ uint32_t ref16(uint32_t r) { return ((r >> 16) & 0x8000u) | (r & 0x7FFFu); }
-__device__ __forceinline__ uint32_t ref32(uint32_t h) {
-  return ((h & 0x8000u) << 16) | (h & 0x7FFFu) | (((h + 1u) >> 16) * 0x7FFF8000u);
-}
-__device__ __forceinline__ uint2 pack_agent(const uint4& v) {
-  return make_uint2(v.x | (ref16(v.y) << 16), ref16(v.z) | (ref16(v.w) << 16));
-}
-__device__ __forceinline__ uint4 unpack_agent(const uint2& w) {
-  return make_uint4(w.x & 0xFFFFu, ref32(w.x >> 16), ref32(w.y & 0xFFFFu), ref32(w.y >> 16));
-}
-
+// (its arenas hold < 32768 ids, the top one unused, so a variable is
+// 0x8000 | id and 0xFFFF is none), which fits more nets per SM.
 // Tier S keeps references inside the kernel in a sign-extended form: variable
 // x is 0xFFFF8000 | x (bit 31 still marks a variable, kNone is still all ones,
 // agents are plain indices), so the 16-bit halves of the 8-byte agent records
-// convert with one sign extension and one mask instead of ref16/ref32. Every
+// convert with one sign extension or one byte permute per port. Every
 // other tier uses the standard form (INET_VAR_BIT | x). Conversions happen only
 // where tier S meets global memory: the input, the residual equations and the
 // arena / normal-form copies.
