@@ -331,3 +331,24 @@ def test_wide_lsystem_against_oracle(n):
     assert print_configuration(res.final) == want.printed()
     assert len(res.loops) == want.loops
     assert [s.interactions for s in res.loops] == [row[0] for row in want.rows]
+
+
+@pytest.mark.parametrize("ctas", [1, 16, 148])
+def test_errors_in_every_single_net_tier(ctas):
+    """LoopCapExceeded / NoRuleForPair from tiers M, C and X as the reference's classes."""
+    loop = parse_program("Loop >< Z => Loop = Z;\nnet : Loop = Z;")
+    with pytest.raises(errors.LoopCapExceeded) as ei:
+        evaluate(loop.net, loop.rules, EngineConfig(max_loops=7, ctas_per_net=ctas))
+    assert ei.value.max_loops == 7
+    bad = parse_program("A >< B => ;\nnet : A = C;")
+    with pytest.raises(errors.NoRuleForPair) as ei:
+        evaluate(bad.net, bad.rules, EngineConfig(ctas_per_net=ctas))
+    assert ei.value.pair == ("A", "C")
+    # a cap that A(3,5)'s loop count exceeds, on a net large enough to use the tier
+    prog = programs.program("ackermann")
+    want = O.run_config(prog.build_input(3, 5), O.rules_for("ackermann"), collect=True)
+    cap = len(want.rows) // 2
+    with pytest.raises(errors.LoopCapExceeded):
+        evaluate(prog.build_input(3, 5), prog.rules, EngineConfig(max_loops=cap, ctas_per_net=ctas))
+    res = evaluate(prog.build_input(3, 5), prog.rules, EngineConfig(max_loops=len(want.rows), ctas_per_net=ctas))
+    assert res.total_interactions == want.interactions
