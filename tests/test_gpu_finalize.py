@@ -133,7 +133,8 @@ def test_native_text_equals_python_printer():
         assert text == print_configuration(res.final), name
 
 
-@pytest.mark.parametrize("name,params", [("lsystem", (20,)), ("ackermann", (3, 7)), ("fibonacci", (14,))])
+@pytest.mark.parametrize("name,params", [("lsystem", (20,)), ("lsystem", (24,)), ("ackermann", (3, 7)),
+                                         ("fibonacci", (14,))])
 def test_host_walk_equals_general_finalize_on_single_nets(name, params):
     prog = programs.program(name)
     nets = [prog.build_input(*params)]
