@@ -50,6 +50,12 @@
 // Reference loop mode code (deferred equations). The rule-set kernels are
 // compiled with and without it: nets whose merges only ever form active pairs
 // (all Ackermann nets) run the smaller kernel and get the same rounds.
+// Per-rule interaction counts (accounting runs): the rule-set kernels are
+// built with or without them (INET_COUNT_RULES 0/1); the prebuilt kernels
+// check at run time.
+#ifndef INET_COUNT_RULES
+#define INET_COUNT_RULES 1
+#endif
 #ifndef INET_EXACT_CODE
 #define INET_EXACT_CODE 1
 #endif
@@ -877,7 +883,7 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
     l = r;
     r = u;
   }
-#ifndef INET_CTIMING
+#if !defined(INET_CTIMING) && INET_COUNT_RULES
   if (c.d->rule_hist) atomicAdd(&c.d->rule_hist[t >> 1], 1u);
 #endif
 #ifdef INET_JIT

@@ -484,10 +484,11 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
   // code style per tier: straight-line cases where the rewrite is issue-bound
   // (S, M, G); a uniform memory phase where remote latency dominates (C)
   const int style = c->jit_style >= 0 ? c->jit_style : (tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0);
-  const auto key = std::make_tuple(tier, threads, style + (c->exact_code ? 16 : 0));
+  const auto key = std::make_tuple(tier, threads, style + (c->exact_code ? 16 : 0) + (c->count_rules ? 32 : 0));
   auto it = c->jit_kernels.find(key);
   if (it != c->jit_kernels.end()) return reinterpret_cast<const void*>(it->second.second);
-  const std::string src = inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style, c->exact_code);
+  const std::string src =
+      inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style, c->exact_code, c->count_rules);
   std::vector<char> cubin;
   if (inetjit::compile_cubin(src, cubin, c->jit_log) != 0) {
     std::fprintf(stderr, "inet_b200: rule-set JIT unavailable, using the prebuilt kernels: %s\n", c->jit_log.c_str());
