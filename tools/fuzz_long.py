@@ -18,7 +18,8 @@ seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 budget_s = float(sys.argv[2]) if len(sys.argv) > 2 else 300
 t0 = time.time()
 stats = {"nets": 0, "exact": 0, "graph": 0, "bad": 0, "single": 0}
-for seed in range(100, 100 + seeds):
+base = int(sys.argv[3]) if len(sys.argv) > 3 else 100
+for seed in range(base, base + seeds):
     if time.time() - t0 > budget_s:
         break
     rng = random.Random(seed)
