@@ -265,3 +265,18 @@ def test_abi_struct_sizes_match_the_library():
     lib.inet_abi_sizes(C.byref(cfg_b), C.byref(st_b))
     assert cfg_b.value == C.sizeof(_native.Cfg)
     assert st_b.value == C.sizeof(_native.NetStats)
+
+
+def test_public_entry_points_without_device_fail_loudly():
+    """No CPU fallback: evaluate / evaluate_batch / evaluate_text raise DeviceError without a GPU."""
+    from conftest import has_gpu
+    from paper_1404_0076_b200 import evaluate, evaluate_batch, evaluate_text, programs as P
+
+    if has_gpu():
+        pytest.skip("a GPU is present")
+    prog = P.program("ackermann")
+    net = prog.build_input(2, 2)
+    for call in (lambda: evaluate(net, prog.rules), lambda: evaluate_batch([net, net], prog.rules),
+                 lambda: evaluate_text(net, prog.rules)):
+        with pytest.raises(errors.DeviceError):
+            call()
