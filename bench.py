@@ -56,6 +56,13 @@ def dist_env():
 
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled during the timed region.
+
+    NVML (pynvml) every 10 ms from a thread, with one sample at entry and one at
+    exit so even a short region is covered; nvidia-smi -lms as the fallback.
+    """
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -63,13 +70,48 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.nvml = None
+        self.samples: list[tuple[float, float, int]] = []  # (sm MHz, max sm MHz, reason bits)
         self.lines: list[str] = []
+        self.stop = threading.Event()
+
+    def _nvml_sample(self):
+        n = self.nvml
+        sm = n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self.handle, n.NVML_CLOCK_SM)
+        try:
+            bits = n.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        except AttributeError:
+            bits = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+        self.samples.append((float(sm), float(mx), int(bits)))
+
+    def _nvml_loop(self):
+        while not self.stop.wait(0.01):
+            try:
+                self._nvml_sample()
+            except Exception:  # noqa: BLE001 - sampling must never break the benchmark
+                return
 
     def __enter__(self):
         try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            # CUDA ordinal -> NVML index (CUDA_VISIBLE_DEVICES may remap)
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._nvml_sample()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except (FileNotFoundError, OSError):
@@ -81,6 +123,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self.t.join(timeout=1)
+            try:
+                self._nvml_sample()
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -90,6 +139,12 @@ class ClockSampler:
 
     def summary(self) -> dict:
         sm, mx, reasons = [], [], set()
+        for s, m, bits in self.samples:
+            sm.append(s)
+            mx.append(m)
+            for name, bit in self.REASONS.items():
+                if bits & bit:
+                    reasons.add(name)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -106,7 +161,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
