@@ -1115,6 +1115,18 @@ int finalize_batch(inet_ctx& c, uint32_t net, uint32_t n_threads) {
     if (net >= c.n_nets) return INET_ERR_ARG;
     return one(net);
   }
+  // nets the device finalized only need their pointers set: no worker threads
+  // for them (spawning 16 threads costs more than the whole loop)
+  uint32_t host_nets = 0;
+  for (uint32_t i = 0; i < c.n_nets; ++i) host_nets += i >= c.dev_rows.size() || c.dev_rows[i] == 0;
+  if (host_nets == 0) {
+    int first = INET_OK;
+    for (uint32_t i = 0; i < c.n_nets; ++i) {
+      const int st = one(i);
+      if (st != INET_OK && first == INET_OK) first = st;
+    }
+    return first;
+  }
   return parallel_for(c.n_nets, n_threads, one);
 }
 
