@@ -438,7 +438,7 @@ def run_ours(args) -> None:
             st = c2.stats(0)
             assert code == _native.OK and st.interactions == golden, (label, st.interactions)
             best = []
-            for _ in range(3):
+            for _ in range(5):
                 flush_l2()
                 best.append(c2.rerun(kk))
             ms = min(best)
@@ -472,7 +472,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=["batch", "a310", "a38", "fib18"], default="batch")
     ap.add_argument("--threads", type=int, default=0, help="CTA size per net (0 = auto)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
