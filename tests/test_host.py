@@ -2,6 +2,7 @@
 benchmark programs, rule-table compiler, flattener, native host finalize and
 the C-ABI export list."""
 
+import os
 import re
 
 import numpy as np
@@ -280,3 +281,37 @@ def test_public_entry_points_without_device_fail_loudly():
                  lambda: evaluate_text(net, prog.rules)):
         with pytest.raises(errors.DeviceError):
             call()
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not present (build container only)")
+def test_install_rebinds_reference_and_accepts_its_objects():
+    """Drop-in boundary on CPU: install() rebinds the reference's evaluate, and the
+    reference's own Configuration / RuleSet objects flatten to exactly the arrays
+    this package's objects give (the device input is the same)."""
+    import importlib
+    import sys as _sys
+
+    if REF_SRC not in _sys.path:
+        _sys.path.insert(0, REF_SRC)
+    inet = importlib.import_module("inet")
+    ref_bench = importlib.import_module("inet.bench")
+    import paper_1404_0076_b200 as b200
+    from paper_1404_0076_b200 import engine, programs as P
+
+    saved = inet.engine.evaluate
+    try:
+        b200.install(inet)
+        assert inet.engine.evaluate is b200.evaluate and inet.evaluate is b200.evaluate
+    finally:
+        inet.engine.evaluate = saved
+        inet.evaluate = saved
+    for name, params in (("ackermann", (2, 3)), ("fibonacci", (7,))):
+        ref_prog = ref_bench.program(name)
+        ours = P.program(name)
+        a = engine.prepare([ref_prog.build_input(*params)], ref_prog.rules)
+        b = engine.prepare([ours.build_input(*params)], ours.rules)
+        for field in ("blob", "agents", "eqs", "iface", "n_vars"):
+            assert np.array_equal(getattr(a, field), getattr(b, field)), (name, field)
