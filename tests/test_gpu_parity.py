@@ -352,3 +352,21 @@ def test_errors_in_every_single_net_tier(ctas):
         evaluate(prog.build_input(3, 5), prog.rules, EngineConfig(max_loops=cap, ctas_per_net=ctas))
     res = evaluate(prog.build_input(3, 5), prog.rules, EngineConfig(max_loops=len(want.rows), ctas_per_net=ctas))
     assert res.total_interactions == want.interactions
+
+
+def test_sharded_batch_gathers_in_input_order():
+    """evaluate_sharded: contiguous shards, one host thread each (here two shards
+    on the one device), results gathered in input order like evaluate_batch."""
+    from paper_1404_0076_b200 import evaluate_sharded
+
+    prog = programs.program("ackermann")
+    rng = random.Random(21)
+    params = [(rng.randint(0, 3), rng.randint(0, 5)) for _ in range(101)]
+    nets = [prog.build_input(m, n) for m, n in params]
+    one = evaluate_batch(nets, prog.rules, EngineConfig(collect_stats=False))
+    two = evaluate_sharded(nets, prog.rules, devices=[0, 0], cfg=EngineConfig(collect_stats=False))
+    assert len(two.results) == len(nets)
+    assert two.total_interactions == one.total_interactions
+    for a, b in zip(one.results, two.results):
+        assert a.total_interactions == b.total_interactions
+        assert print_configuration(a.final) == print_configuration(b.final)
