@@ -140,6 +140,14 @@ int inet_set_jit(inet_ctx* ctx, int mode);
  * a device; returns INET_OK or INET_ERR_UNSUPPORTED with the NVRTC log. */
 int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t threads, char* log, size_t log_len);
 
+/* Build time: compile the specialised kernel of (rule blob, tier, CTA size)
+ * into the package's kernels/ directory next to the library, where every
+ * later process finds it without running NVRTC (the shipped programs are
+ * precompiled by the package build). flags: bit 0 reference-loop code
+ * (deferred equations), bit 1 per-rule counters. */
+int inet_jit_precompile(const uint32_t* blob, size_t n_words, int tier, uint32_t threads, uint32_t flags, char* log,
+                        size_t log_len);
+
 /* Upload a compiled rule set. Replaces RuleSet.lookup / find_rule / instantiate
  * (core.py:241-242, 281-312): the per-equation dictionary lookup and tree
  * rebuild become one table lookup and a template expansion on the device. */

@@ -29,6 +29,7 @@ EXPORTS = (
     "inet_rules_load",
     "inet_set_jit",
     "inet_jit_compile",
+    "inet_jit_precompile",
     "inet_batch_load",
     "inet_batch_reduce",
     "inet_batch_rerun",
@@ -105,6 +106,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             "inet_rules_load": (C.c_int, [C.c_void_p, _u32p, C.c_size_t]),
             "inet_set_jit": (C.c_int, [C.c_void_p, C.c_int]),
             "inet_jit_compile": (C.c_int, [_u32p, C.c_size_t, C.c_int, C.c_uint32, C.c_char_p, C.c_size_t]),
+            "inet_jit_precompile": (
+                C.c_int, [_u32p, C.c_size_t, C.c_int, C.c_uint32, C.c_uint32, C.c_char_p, C.c_size_t]),
             "inet_batch_load": (C.c_int, [C.c_void_p, C.c_uint32, _u32p, _u64p, _u32p, _u64p, _u32p, _u64p, _u32p]),
             "inet_batch_reduce": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
             "inet_batch_rerun": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
@@ -348,6 +351,19 @@ def jit_compile(blob: np.ndarray, tier: int = 1, threads: int = 1024) -> tuple[i
     blob = np.ascontiguousarray(blob, dtype=np.uint32)
     log = C.create_string_buffer(1 << 16)
     code = lib.inet_jit_compile(_ptr(blob), blob.size, tier, threads, log, len(log))
+    return code, log.value.decode(errors="replace")
+
+
+TIER_S, TIER_M, TIER_G, TIER_C, TIER_X = 0, 1, 2, 3, 4
+
+
+def jit_precompile(blob: np.ndarray, tier: int, threads: int, exact_code: bool, count_rules: bool) -> tuple[int, str]:
+    """Compile one kernel variant into the package's kernels/ directory (build time)."""
+    lib = load_library()
+    blob = np.ascontiguousarray(blob, dtype=np.uint32)
+    log = C.create_string_buffer(1 << 16)
+    flags = (1 if exact_code else 0) | (2 if count_rules else 0)
+    code = lib.inet_jit_precompile(_ptr(blob), blob.size, tier, threads, flags, log, len(log))
     return code, log.value.decode(errors="replace")
 
 

@@ -832,13 +832,13 @@ __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uin
       return false;
     }
   }
-  // ring entries loaded unconditionally (masked indices are always in range) so
-  // the loads issue back to back instead of one predicated block per id
+  // only the claimed ring entries are read (predicated loads, still issued back
+  // to back): an entry past the claim may be being written by a freer this round
   uint32_t rv[MF], ra[MX];
 #pragma unroll
-  for (uint32_t j = 0; j < MF; ++j) rv[j] = c.vring[(c.lo_v + tv + j) & c.vmask];
+  for (uint32_t j = 0; j < MF; ++j) rv[j] = j < gv ? static_cast<uint32_t>(c.vring[(c.lo_v + tv + j) & c.vmask]) : 0u;
 #pragma unroll
-  for (uint32_t j = 0; j < MX; ++j) ra[j] = c.aring[(c.lo_a + ta + j) & c.amask];
+  for (uint32_t j = 0; j < MX; ++j) ra[j] = j < ga ? static_cast<uint32_t>(c.aring[(c.lo_a + ta + j) & c.amask]) : 0u;
 #pragma unroll
   for (uint32_t j = 0; j < MF; ++j) f[j] = vtag<kTier>() | (j < gv ? rv[j] : bump_var(c, bv + (j - gv)));
 #pragma unroll
@@ -1247,12 +1247,12 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   if (!fits) {
     stop = true;
     stop_err = INET_ERR_ARENA;
+  } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207), even for the no-op loop
+    stop = true;
+    stop_err = INET_ERR_LOOP_CAP;
   } else if (d.n_in_eqs == 0) {  // one no-op loop (engine.py:222-223)
     stop = true;
     if (threadIdx.x == 0 && d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
-  } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207)
-    stop = true;
-    stop_err = INET_ERR_LOOP_CAP;
   }
   __syncthreads();
   c.failed = false;
@@ -1410,17 +1410,17 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     nd = INET_EXACT_CODE ? k.dcount : 0u;
     if (round_failed) {
       stop = true;
+    } else if (!INET_EXACT_CODE && sh.detect_vh && k.vh) {
+      stop = true;  // the host reruns the net with reference-loop code
+      stop_err = kNeedExact;
+    } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207 (checked before every loop, the no-op one too)
+      stop = true;
+      stop_err = INET_ERR_LOOP_CAP;
     } else if (q == 0 && nd == 0) {
       // the trailing no-op loop the reference records (engine.py:222-223)
       stop = true;
       if (threadIdx.x == 0 && d.stats && r < d.cap_rounds)
         d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
-    } else if (!INET_EXACT_CODE && sh.detect_vh && k.vh) {
-      stop = true;  // the host reruns the net with reference-loop code
-      stop_err = kNeedExact;
-    } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207
-      stop = true;
-      stop_err = INET_ERR_LOOP_CAP;
     } else if (kTier == kTierM && sh.promote_ints && (tot_q += q) >= sh.promote_ints) {
       stop = true;  // a large net: the host hands it over to a cluster
       stop_err = kPromote;
@@ -1683,12 +1683,12 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   if (!fits) {
     stop = true;
     stop_err = INET_ERR_ARENA;
+  } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207), even for the no-op loop
+    stop = true;
+    stop_err = INET_ERR_LOOP_CAP;
   } else if (N == 0) {  // one no-op loop (engine.py:222-223)
     stop = true;
     if (writer && d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
-  } else if (sh.max_rounds == 0) {  // loop 1 > max_loops (engine.py:205-207)
-    stop = true;
-    stop_err = INET_ERR_LOOP_CAP;
   }
   for (uint32_t r = 1; !stop; ++r) {
     RoundCtr* cur = &ctr3[r % 3];
@@ -1896,11 +1896,11 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
     } else if (vh_any) {
       stop = true;  // the host reruns the net with reference-loop code
       stop_err = kNeedExact;
-    } else if (total == 0 && !deferred_any) {
-      stop = true;  // the trailing no-op loop the reference records (engine.py:222-223)
-    } else if (rb + r + 1 > sh.max_rounds) {  // engine.py:205-207
+    } else if (rb + r + 1 > sh.max_rounds) {  // engine.py:205-207 (the no-op loop too)
       stop = true;
       stop_err = INET_ERR_LOOP_CAP;
+    } else if (total == 0 && !deferred_any) {
+      stop = true;  // the trailing no-op loop the reference records (engine.py:222-223)
     }
   }
 #ifdef INET_CTIMING
@@ -2089,12 +2089,12 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
   if (!fits) {
     stop = true;
     stop_err = INET_ERR_ARENA;
-  } else if (d.n_in_eqs == 0) {
-    stop = true;
-    if (lead && d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
   } else if (sh.max_rounds == 0) {
     stop = true;
     stop_err = INET_ERR_LOOP_CAP;
+  } else if (d.n_in_eqs == 0) {
+    stop = true;
+    if (lead && d.stats && d.cap_rounds) d.stats[0] = make_uint4(0, 0, 0, 0);
   }
   __shared__ uint32_t red3[3];
   __shared__ uint32_t scan_scratch[34];
@@ -2185,15 +2185,15 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
     n = q;
     if (round_failed) {
       stop = true;
-    } else if (q == 0) {
-      stop = true;
-      if (lead && d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
     } else if (sh.detect_vh && k.vh) {
       stop = true;
       stop_err = kNeedExact;
-    } else if (r + 1 > sh.max_rounds) {
+    } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207 (the no-op loop too)
       stop = true;
       stop_err = INET_ERR_LOOP_CAP;
+    } else if (q == 0) {
+      stop = true;
+      if (lead && d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
     } else if (q > c.cap_queue) {
       stop = true;
       stop_err = INET_ERR_ARENA;

@@ -5,6 +5,7 @@
 // does no cudaMalloc. A batch of nets is laid out as per-net slabs of equal
 // capacity; one CTA reduces one net (device.cuh), the grid covers the batch.
 // If any net overflows its arena the batch is re-run with doubled capacity.
+#include <new>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -183,6 +184,7 @@ struct inet_ctx {
   std::vector<uint32_t> h_hist;
   uint64_t io_h2d = 0, io_d2h = 0;
   uint32_t cap_agents = 0, cap_vars = 0, cap_queue = 0, cap_rounds = 0;
+  uint32_t rows_hint = 0;  // LoopStats rows per net the last run needed (see rows_cap)
   int tier = kTierG;  // tier of the last successful run
   uint32_t cluster_g = 1;  // CTAs per net of the last run (tier C)
   // a single net promoted from one CTA to a cluster: the tier M prefix that
@@ -208,7 +210,8 @@ struct inet_ctx {
   PinnedU32 h_agents;                 // per-net slab prefixes [n_nets * agent_pitch * 4]
   PinnedU32 h_resid;                  // [n_nets * resid_pitch * 2]
   uint32_t agent_pitch = 0, resid_pitch = 0;
-  std::vector<uint32_t> h_rounds;     // [n_nets * cap_rounds * 4]
+  std::vector<uint32_t> h_rounds;     // [n_nets * rows_pitch * 4]
+  uint32_t rows_pitch = 1;
   std::vector<inethost::NormalForm> results;
   std::vector<uint8_t> finalized;
   // rule-set specialised kernels (jit.cpp), keyed by (tier, block size)
@@ -268,25 +271,31 @@ void inet_abi_sizes(size_t* cfg_bytes, size_t* stats_bytes) {
 }
 
 int inet_ctx_create(int device, inet_ctx** out) {
-  if (!out) return INET_ERR_ARG;
-  *out = nullptr;
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return INET_ERR_NO_DEVICE;
-  if (device < 0 || device >= n) return INET_ERR_ARG;
-  CUDA_TRY(cudaSetDevice(device));
-  auto* c = new inet_ctx();
-  c->device = device;
-  if (const char* e = std::getenv("INET_B200_JIT")) c->jit_mode = std::atoi(e);
-  if (const char* e = std::getenv("INET_B200_JITSTYLE")) c->jit_style = std::atoi(e);
-  if (const char* e = std::getenv("INET_B200_PROMOTE")) c->promote_ints = static_cast<uint32_t>(std::atol(e));
-  if (const char* e = std::getenv("INET_B200_DEVFINAL")) c->dev_final = std::atoi(e) != 0;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
-    delete c;
-    return INET_ERR_CUDA;
+  try {
+    if (!out) return INET_ERR_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return INET_ERR_NO_DEVICE;
+    if (device < 0 || device >= n) return INET_ERR_ARG;
+    CUDA_TRY(cudaSetDevice(device));
+    auto* c = new inet_ctx();
+    c->device = device;
+    if (const char* e = std::getenv("INET_B200_JIT")) c->jit_mode = std::atoi(e);
+    if (const char* e = std::getenv("INET_B200_JITSTYLE")) c->jit_style = std::atoi(e);
+    if (const char* e = std::getenv("INET_B200_PROMOTE")) c->promote_ints = static_cast<uint32_t>(std::atol(e));
+    if (const char* e = std::getenv("INET_B200_DEVFINAL")) c->dev_final = std::atoi(e) != 0;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+      delete c;
+      return INET_ERR_CUDA;
+    }
+    *out = c;
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  *out = c;
-  return INET_OK;
 }
 
 void inet_ctx_destroy(inet_ctx* c) {
@@ -303,65 +312,83 @@ void inet_ctx_destroy(inet_ctx* c) {
 }
 
 int inet_device_info(inet_ctx* c, int* sm_count, int* clock_khz, char* name, size_t name_len) {
-  if (!c) return INET_ERR_ARG;
-  cudaDeviceProp prop;
-  CUDA_TRY(cudaGetDeviceProperties(&prop, c->device));
-  if (sm_count) *sm_count = prop.multiProcessorCount;
-  if (clock_khz) cudaDeviceGetAttribute(clock_khz, cudaDevAttrClockRate, c->device);
-  if (name && name_len) {
-    std::strncpy(name, prop.name, name_len - 1);
-    name[name_len - 1] = 0;
+  try {
+    if (!c) return INET_ERR_ARG;
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, c->device));
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    if (clock_khz) cudaDeviceGetAttribute(clock_khz, cudaDevAttrClockRate, c->device);
+    if (name && name_len) {
+      std::strncpy(name, prop.name, name_len - 1);
+      name[name_len - 1] = 0;
+    }
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  return INET_OK;
 }
 
 int inet_rules_load(inet_ctx* c, const uint32_t* blob, size_t n_words) {
-  if (!c || !blob || n_words < 4) return INET_ERR_ARG;
-  int st = inethost::validate_rule_blob(blob, n_words);
-  if (st != INET_OK) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
-  if (c->blob.size() != n_words || !std::equal(c->blob.begin(), c->blob.end(), blob)) {
-    for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
-    c->jit_kernels.clear();
+  try {
+    if (!c || !blob || n_words < 4) return INET_ERR_ARG;
+    int st = inethost::validate_rule_blob(blob, n_words);
+    if (st != INET_OK) return st;
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->blob.size() != n_words || !std::equal(c->blob.begin(), c->blob.end(), blob)) {
+      for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
+      c->jit_kernels.clear();
+    }
+    c->blob.assign(blob, blob + n_words);
+    c->n_labels = blob[1];
+    c->n_rules = blob[2];
+    c->smem_bytes = static_cast<uint32_t>((n_words - 4) * 4);
+    if (c->d_blob.ensure(n_words * 4)) return INET_ERR_CUDA;
+    CUDA_TRY(cudaMemcpyAsync(c->d_blob.p, blob, n_words * 4, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  c->blob.assign(blob, blob + n_words);
-  c->n_labels = blob[1];
-  c->n_rules = blob[2];
-  c->smem_bytes = static_cast<uint32_t>((n_words - 4) * 4);
-  if (c->d_blob.ensure(n_words * 4)) return INET_ERR_CUDA;
-  CUDA_TRY(cudaMemcpyAsync(c->d_blob.p, blob, n_words * 4, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  return INET_OK;
 }
 
 int inet_batch_load(inet_ctx* c, uint32_t n_nets, const uint32_t* agents, const uint64_t* agent_off,
                     const uint32_t* eqs, const uint64_t* eq_off, const uint32_t* iface, const uint64_t* iface_off,
                     const uint32_t* n_vars) {
-  if (!c || n_nets == 0 || !agent_off || !eq_off || !iface_off || !n_vars) return INET_ERR_ARG;
-  if (c->blob.empty()) return INET_ERR_STATE;
-  c->n_nets = n_nets;
-  c->agent_off.assign(agent_off, agent_off + n_nets + 1);
-  c->eq_off.assign(eq_off, eq_off + n_nets + 1);
-  c->iface_off.assign(iface_off, iface_off + n_nets + 1);
-  c->n_vars.assign(n_vars, n_vars + n_nets);
-  c->agents.assign(agents, agents + 4 * agent_off[n_nets]);
-  c->eqs.assign(eqs, eqs + 2 * eq_off[n_nets]);
-  c->iface.assign(iface, iface + iface_off[n_nets]);
-  c->max_in_agents = c->max_in_eqs = c->max_in_vars = 0;
-  for (uint32_t i = 0; i < n_nets; ++i) {
-    const uint64_t na = agent_off[i + 1] - agent_off[i], ne = eq_off[i + 1] - eq_off[i];
-    if (na >= INET_VAR_BIT || ne >= INET_VAR_BIT || n_vars[i] >= INET_VAR_BIT - 1) return INET_ERR_UNSUPPORTED;
-    c->max_in_agents = std::max<uint32_t>(c->max_in_agents, static_cast<uint32_t>(na));
-    c->max_in_eqs = std::max<uint32_t>(c->max_in_eqs, static_cast<uint32_t>(ne));
-    c->max_in_vars = std::max<uint32_t>(c->max_in_vars, n_vars[i]);
+  try {
+    if (!c || n_nets == 0 || !agent_off || !eq_off || !iface_off || !n_vars) return INET_ERR_ARG;
+    if (c->blob.empty()) return INET_ERR_STATE;
+    c->n_nets = n_nets;
+    c->agent_off.assign(agent_off, agent_off + n_nets + 1);
+    c->eq_off.assign(eq_off, eq_off + n_nets + 1);
+    c->iface_off.assign(iface_off, iface_off + n_nets + 1);
+    c->n_vars.assign(n_vars, n_vars + n_nets);
+    c->agents.assign(agents, agents + 4 * agent_off[n_nets]);
+    c->eqs.assign(eqs, eqs + 2 * eq_off[n_nets]);
+    c->iface.assign(iface, iface + iface_off[n_nets]);
+    c->max_in_agents = c->max_in_eqs = c->max_in_vars = 0;
+    for (uint32_t i = 0; i < n_nets; ++i) {
+      const uint64_t na = agent_off[i + 1] - agent_off[i], ne = eq_off[i + 1] - eq_off[i];
+      if (na >= INET_VAR_BIT || ne >= INET_VAR_BIT || n_vars[i] >= INET_VAR_BIT - 1) return INET_ERR_UNSUPPORTED;
+      c->max_in_agents = std::max<uint32_t>(c->max_in_agents, static_cast<uint32_t>(na));
+      c->max_in_eqs = std::max<uint32_t>(c->max_in_eqs, static_cast<uint32_t>(ne));
+      c->max_in_vars = std::max<uint32_t>(c->max_in_vars, n_vars[i]);
+    }
+    int st = inethost::validate_nets(*c);
+    if (st != INET_OK) return st;
+    c->input_resident = false;
+    c->reduced = false;
+    c->results.clear();
+    c->finalized.clear();
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  int st = inethost::validate_nets(*c);
-  if (st != INET_OK) return st;
-  c->input_resident = false;
-  c->reduced = false;
-  c->results.clear();
-  c->finalized.clear();
-  return INET_OK;
 }
 
 }  // extern "C"
@@ -601,7 +628,40 @@ Shape base_shape(const inet_ctx* c, uint32_t max_loops) {
   return sh;
 }
 
+// Per-net capacity of the LoopStats rows buffer. The reference keeps one row
+// per loop (up to max_loops + 1); a batch of nets with the default cap of a
+// million loops would need tens of GB, so the first attempt gets a share of a
+// fixed budget (2^24 rows = 256 MB over all nets, at least 1,024 per net) and
+// a run whose nets needed more rows is repeated once with exactly that many
+// (c->rows_hint, set by run()). Rows past 2^22 per net are not recorded.
+constexpr uint32_t kRowsBudget = 1u << 24;
+constexpr uint32_t kRowsMax = 1u << 22;
+
+uint32_t rows_cap(const inet_ctx* c, uint32_t max_loops) {
+  const uint32_t want = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(max_loops) + 1u, kRowsMax));
+  const uint32_t share = std::max<uint32_t>(1024u, kRowsBudget / std::max<uint32_t>(c->n_nets, 1u));
+  return std::min(want, std::max(share, c->rows_hint));
+}
+
+int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch);
+
 int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
+  if (!c) return INET_ERR_STATE;
+  c->rows_hint = 0;
+  int st = run_once(c, cfg, device_ms, fetch);
+  if (c->collect_stats && !c->stats.empty()) {
+    uint32_t need = 0;
+    for (const auto& s : c->stats) need = std::max(need, s.rounds);
+    need = std::min(need, kRowsMax);
+    if (need > c->cap_rounds) {  // some net's rows did not fit: once more with room for all of them
+      c->rows_hint = need;
+      st = run_once(c, cfg, device_ms, fetch);
+    }
+  }
+  return st;
+}
+
+int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   if (!c || c->n_nets == 0 || c->blob.empty()) return INET_ERR_STATE;
   CUDA_TRY(cudaSetDevice(c->device));
   if (!c->input_resident) {
@@ -611,8 +671,7 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   const uint32_t max_loops = cfg ? cfg->max_loops : 1000000u;
   c->collect_stats = cfg && cfg->collect_stats;
   c->count_rules = cfg && cfg->count_rules;
-  uint32_t cap_rounds = 0;
-  if (c->collect_stats) cap_rounds = std::min<uint32_t>(max_loops + 1u, 1u << 22);
+  const uint32_t cap_rounds = c->collect_stats ? rows_cap(c, max_loops) : 0u;
   const uint32_t retries = cfg && cfg->max_retries ? cfg->max_retries : 8;
   float ms = 0;
   c->ctl.assign(c->n_nets, NetCtl{});
@@ -854,9 +913,10 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     if (c->collect_stats) {
       uint32_t max_r = 0;
       for (auto& s : c->stats) max_r = std::max(max_r, std::min(s.rounds, c->cap_rounds));
-      c->h_rounds.resize(size_t(c->n_nets) * c->cap_rounds * 4);
+      c->rows_pitch = std::max(max_r, 1u);  // host copy: only the rows some net used
+      c->h_rounds.resize(size_t(c->n_nets) * c->rows_pitch * 4);
       if (max_r)
-        CUDA_TRY(cudaMemcpy2DAsync(c->h_rounds.data(), size_t(c->cap_rounds) * 16, c->d_stats.p,
+        CUDA_TRY(cudaMemcpy2DAsync(c->h_rounds.data(), size_t(c->rows_pitch) * 16, c->d_stats.p,
                                    size_t(c->cap_rounds) * 16, size_t(max_r) * 16, c->n_nets,
                                    cudaMemcpyDeviceToHost, c->stream));
     }
@@ -880,173 +940,267 @@ int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
 extern "C" {
 
 int inet_batch_reduce(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
-  if (!c) return INET_ERR_ARG;
-  c->input_resident = false;
-  c->io_h2d = c->io_d2h = 0;
-  return run(c, cfg, device_ms, true);
+  try {
+    if (!c) return INET_ERR_ARG;
+    c->input_resident = false;
+    c->io_h2d = c->io_d2h = 0;
+    return run(c, cfg, device_ms, true);
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
-  if (!c || !c->reduced) return INET_ERR_STATE;
-  // same tier, shape and capacities as the successful run: no growth expected
-  inet_cfg k = cfg ? *cfg : inet_cfg{1000000u, 0, 0, 0, 0, 0, 0, 0};
-  c->count_rules = k.count_rules != 0;
-  CUDA_TRY(cudaSetDevice(c->device));
-  const uint32_t cap_rounds = (k.collect_stats) ? std::min<uint32_t>(k.max_loops + 1u, 1u << 22) : 0;
-  float pre_ms = 0;
-  if (c->promoted) {
-    // replay the single-CTA prefix up to the promotion threshold, then the cluster run
-    const uint32_t ca = c->cap_agents, cv = c->cap_vars, cq = c->cap_queue, cd = c->cap_def;
-    c->cap_def = c->promo_cap_def;
-    c->resume.on = false;
-    int st = layout(c, kPromoCapAgents, kPromoCapVars, kPromoCapQueue, cap_rounds);
+  try {
+    if (!c || !c->reduced) return INET_ERR_STATE;
+    // same tier, shape and capacities as the successful run: no growth expected
+    inet_cfg k = cfg ? *cfg : inet_cfg{1000000u, 0, 0, 0, 0, 0, 0, 0};
+    c->count_rules = k.count_rules != 0;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const uint32_t cap_rounds = k.collect_stats ? rows_cap(c, k.max_loops) : 0u;
+    float pre_ms = 0;
+    if (c->promoted) {
+      // replay the single-CTA prefix up to the promotion threshold, then the cluster run
+      const uint32_t ca = c->cap_agents, cv = c->cap_vars, cq = c->cap_queue, cd = c->cap_def;
+      c->cap_def = c->promo_cap_def;
+      c->resume.on = false;
+      int st = layout(c, kPromoCapAgents, kPromoCapVars, kPromoCapQueue, cap_rounds);
+      if (st) return st;
+      Shape ps = c->promo_shape;
+      ps.max_rounds = k.max_loops;
+      st = launch(c, &k, ps, kTierM, &pre_ms);
+      if (st) return st;
+      NetCtl m;
+      CUDA_TRY(cudaMemcpy(&m, c->d_ctl.p, sizeof(NetCtl), cudaMemcpyDeviceToHost));
+      if (m.err != inetdev::kPromote) return INET_ERR_STATE;
+      set_resume(c, m);
+      c->cap_def = cd;
+      c->cap_agents = ca;
+      c->cap_vars = cv;
+      c->cap_queue = cq;
+    }
+    c->grid_tier = c->tier == inetdev::kTierX;
+    int st = layout(c, c->cap_agents, c->cap_vars, c->cap_queue, cap_rounds);
+    c->grid_tier = false;
     if (st) return st;
-    Shape ps = c->promo_shape;
-    ps.max_rounds = k.max_loops;
-    st = launch(c, &k, ps, kTierM, &pre_ms);
+    Shape sh = c->shape;
+    sh.max_rounds = k.max_loops;
+    float ms = 0;
+    st = launch(c, &k, sh, c->tier, &ms);
     if (st) return st;
-    NetCtl m;
-    CUDA_TRY(cudaMemcpy(&m, c->d_ctl.p, sizeof(NetCtl), cudaMemcpyDeviceToHost));
-    if (m.err != inetdev::kPromote) return INET_ERR_STATE;
-    set_resume(c, m);
-    c->cap_def = cd;
-    c->cap_agents = ca;
-    c->cap_vars = cv;
-    c->cap_queue = cq;
+    if (device_ms) *device_ms = ms + pre_ms;
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  c->grid_tier = c->tier == inetdev::kTierX;
-  int st = layout(c, c->cap_agents, c->cap_vars, c->cap_queue, cap_rounds);
-  c->grid_tier = false;
-  if (st) return st;
-  Shape sh = c->shape;
-  sh.max_rounds = k.max_loops;
-  float ms = 0;
-  st = launch(c, &k, sh, c->tier, &ms);
-  if (st) return st;
-  if (device_ms) *device_ms = ms + pre_ms;
-  return INET_OK;
 }
 
 int inet_batch_stats(inet_ctx* c, uint32_t net, inet_net_stats* out) {
-  if (!c || !out) return INET_ERR_ARG;
-  if (!c->reduced) return INET_ERR_STATE;
-  if (net >= c->n_nets) return INET_ERR_ARG;
-  *out = c->stats[net];
-  return INET_OK;
+  try {
+    if (!c || !out) return INET_ERR_ARG;
+    if (!c->reduced) return INET_ERR_STATE;
+    if (net >= c->n_nets) return INET_ERR_ARG;
+    *out = c->stats[net];
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t threads, char* log, size_t log_len) {
-  if (!blob || n_words < 4) return INET_ERR_ARG;
-  if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
-  std::vector<char> cubin;
-  std::string msg;
-  int style = tier == kTierC ? 1 : 0;
-  if (const char* e = std::getenv("INET_B200_JITSTYLE")) style = std::atoi(e);
-  bool exact_code = true;
-  if (const char* e = std::getenv("INET_B200_EXACTCODE")) exact_code = std::atoi(e) != 0;
-  const int rc =
-      inetjit::compile_cubin(inetjit::kernel_source(blob, n_words, tier, threads, style, exact_code), cubin, msg);
-  if (log && log_len) {
-    std::strncpy(log, msg.c_str(), log_len - 1);
-    log[log_len - 1] = 0;
+  try {
+    if (!blob || n_words < 4) return INET_ERR_ARG;
+    if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
+    std::vector<char> cubin;
+    std::string msg;
+    int style = tier == kTierC ? 1 : 0;
+    if (const char* e = std::getenv("INET_B200_JITSTYLE")) style = std::atoi(e);
+    bool exact_code = true;
+    if (const char* e = std::getenv("INET_B200_EXACTCODE")) exact_code = std::atoi(e) != 0;
+    const int rc =
+        inetjit::compile_cubin(inetjit::kernel_source(blob, n_words, tier, threads, style, exact_code), cubin, msg);
+    if (log && log_len) {
+      std::strncpy(log, msg.c_str(), log_len - 1);
+      log[log_len - 1] = 0;
+    }
+    return rc == 0 ? INET_OK : INET_ERR_UNSUPPORTED;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  return rc == 0 ? INET_OK : INET_ERR_UNSUPPORTED;
+}
+
+int inet_jit_precompile(const uint32_t* blob, size_t n_words, int tier, uint32_t threads, uint32_t flags, char* log,
+                        size_t log_len) {
+  try {
+    if (!blob || n_words < 4) return INET_ERR_ARG;
+    if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
+    if (tier < kTierS || tier > inetdev::kTierX) return INET_ERR_ARG;
+    const int style = tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0;  // as jit_kernel picks it
+    std::string msg;
+    const int rc = inetjit::precompile(
+        inetjit::kernel_source(blob, n_words, tier, threads, style, (flags & 1u) != 0, (flags & 2u) != 0), msg);
+    if (log && log_len) {
+      std::strncpy(log, msg.c_str(), log_len - 1);
+      log[log_len - 1] = 0;
+    }
+    return rc == 0 ? INET_OK : INET_ERR_UNSUPPORTED;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 int inet_set_jit(inet_ctx* c, int mode) {
-  if (!c) return INET_ERR_ARG;
-  c->jit_mode = mode ? 1 : 0;
-  return INET_OK;
+  try {
+    if (!c) return INET_ERR_ARG;
+    c->jit_mode = mode ? 1 : 0;
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 int inet_batch_rule_counts(inet_ctx* c, uint32_t net, uint64_t* counts, uint32_t n_rules) {
-  if (!c || !counts) return INET_ERR_ARG;
-  if (!c->reduced || !c->count_rules || c->h_hist.empty()) return INET_ERR_STATE;
-  if (net >= c->n_nets) return INET_ERR_ARG;
-  const uint32_t R = hist_stride(c);
-  for (uint32_t r = 0; r < n_rules; ++r) counts[r] = r < R ? c->h_hist[size_t(net) * R + r] : 0;
-  return INET_OK;
+  try {
+    if (!c || !counts) return INET_ERR_ARG;
+    if (!c->reduced || !c->count_rules || c->h_hist.empty()) return INET_ERR_STATE;
+    if (net >= c->n_nets) return INET_ERR_ARG;
+    const uint32_t R = hist_stride(c);
+    for (uint32_t r = 0; r < n_rules; ++r) counts[r] = r < R ? c->h_hist[size_t(net) * R + r] : 0;
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 int inet_batch_io_bytes(inet_ctx* c, uint64_t* h2d, uint64_t* d2h) {
-  if (!c) return INET_ERR_ARG;
-  if (h2d) *h2d = c->io_h2d;
-  if (d2h) *d2h = c->io_d2h;
-  return INET_OK;
+  try {
+    if (!c) return INET_ERR_ARG;
+    if (h2d) *h2d = c->io_h2d;
+    if (d2h) *d2h = c->io_d2h;
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 int inet_batch_totals(inet_ctx* c, uint64_t* interactions, uint64_t* communications, uint32_t* max_rounds,
                       uint32_t* n_failed) {
-  if (!c) return INET_ERR_ARG;
-  if (!c->reduced) return INET_ERR_STATE;
-  uint64_t ti = 0, tc = 0;
-  uint32_t mr = 0, nf = 0;
-  for (auto& s : c->stats) {
-    ti += s.interactions;
-    tc += s.communications;
-    mr = std::max(mr, s.rounds);
-    nf += s.status != INET_OK;
+  try {
+    if (!c) return INET_ERR_ARG;
+    if (!c->reduced) return INET_ERR_STATE;
+    uint64_t ti = 0, tc = 0;
+    uint32_t mr = 0, nf = 0;
+    for (auto& s : c->stats) {
+      ti += s.interactions;
+      tc += s.communications;
+      mr = std::max(mr, s.rounds);
+      nf += s.status != INET_OK;
+    }
+    if (interactions) *interactions = ti;
+    if (communications) *communications = tc;
+    if (max_rounds) *max_rounds = mr;
+    if (n_failed) *n_failed = nf;
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  if (interactions) *interactions = ti;
-  if (communications) *communications = tc;
-  if (max_rounds) *max_rounds = mr;
-  if (n_failed) *n_failed = nf;
-  return INET_OK;
 }
 
 int inet_batch_rounds(inet_ctx* c, uint32_t net, uint32_t* rows, uint32_t* n_rows) {
-  if (!c || !n_rows) return INET_ERR_ARG;
-  if (!c->reduced) return INET_ERR_STATE;
-  if (net >= c->n_nets) return INET_ERR_ARG;
-  if (!c->collect_stats) {
-    *n_rows = 0;
+  try {
+    if (!c || !n_rows) return INET_ERR_ARG;
+    if (!c->reduced) return INET_ERR_STATE;
+    if (net >= c->n_nets) return INET_ERR_ARG;
+    if (!c->collect_stats) {
+      *n_rows = 0;
+      return INET_OK;
+    }
+    const uint32_t n = std::min(c->stats[net].rounds, c->cap_rounds);
+    if (!rows) {
+      *n_rows = n;
+      return INET_OK;
+    }
+    const uint32_t m = std::min(n, *n_rows);
+    std::memcpy(rows, c->h_rounds.data() + size_t(net) * c->rows_pitch * 4, size_t(m) * 16);
+    *n_rows = m;
     return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  const uint32_t n = std::min(c->stats[net].rounds, c->cap_rounds);
-  if (!rows) {
-    *n_rows = n;
-    return INET_OK;
-  }
-  const uint32_t m = std::min(n, *n_rows);
-  std::memcpy(rows, c->h_rounds.data() + size_t(net) * c->cap_rounds * 4, size_t(m) * 16);
-  *n_rows = m;
-  return INET_OK;
 }
 
 int inet_batch_finalize(inet_ctx* c, uint32_t net, uint32_t n_threads) {
-  if (!c) return INET_ERR_ARG;
-  if (!c->reduced) return INET_ERR_STATE;
-  return inethost::finalize_batch(*c, net, n_threads);
+  try {
+    if (!c) return INET_ERR_ARG;
+    if (!c->reduced) return INET_ERR_STATE;
+    return inethost::finalize_batch(*c, net, n_threads);
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 int inet_batch_print(inet_ctx* c, uint32_t net, const char* const* names, const uint8_t* arity, uint32_t n_labels,
                      char* buf, size_t cap, size_t* len) {
-  if (!c || !len || (n_labels && (!names || !arity))) return INET_ERR_ARG;
-  if (!c->reduced || net >= c->n_nets || !c->finalized[net]) return INET_ERR_STATE;
-  if (c->text_net != net) {
-    const inethost::NormalForm& nf = c->results[net];
-    c->text_net = INET_NONE;
-    const int st = inethost::print_flat(nf.agent_data(), nf.n_agents(), nf.iface.data(),
-                                        static_cast<uint32_t>(nf.iface.size()), nf.eqs.data(),
-                                        static_cast<uint32_t>(nf.eqs.size() / 2), names, arity, n_labels, c->text);
-    if (st) return st;
-    c->text_net = net;
+  try {
+    if (!c || !len || (n_labels && (!names || !arity))) return INET_ERR_ARG;
+    if (!c->reduced || net >= c->n_nets || !c->finalized[net]) return INET_ERR_STATE;
+    if (c->text_net != net) {
+      const inethost::NormalForm& nf = c->results[net];
+      c->text_net = INET_NONE;
+      const int st = inethost::print_flat(nf.agent_data(), nf.n_agents(), nf.iface.data(),
+                                          static_cast<uint32_t>(nf.iface.size()), nf.eqs.data(),
+                                          static_cast<uint32_t>(nf.eqs.size() / 2), names, arity, n_labels, c->text);
+      if (st) return st;
+      c->text_net = net;
+    }
+    return inethost::copy_text(c->text, buf, cap, len);
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
   }
-  return inethost::copy_text(c->text, buf, cap, len);
 }
 
 int inet_batch_result(inet_ctx* c, uint32_t net, const uint32_t** agents, uint32_t* n_agents, const uint32_t** iface,
                       uint32_t* n_iface, const uint32_t** eqs, uint32_t* n_eqs) {
-  if (!c) return INET_ERR_ARG;
-  if (!c->reduced || net >= c->n_nets || !c->finalized[net]) return INET_ERR_STATE;
-  const inethost::NormalForm& nf = c->results[net];
-  if (agents) *agents = nf.agent_data();
-  if (n_agents) *n_agents = nf.n_agents();
-  if (iface) *iface = nf.iface.data();
-  if (n_iface) *n_iface = static_cast<uint32_t>(nf.iface.size());
-  if (eqs) *eqs = nf.eqs.data();
-  if (n_eqs) *n_eqs = static_cast<uint32_t>(nf.eqs.size() / 2);
-  return INET_OK;
+  try {
+    if (!c) return INET_ERR_ARG;
+    if (!c->reduced || net >= c->n_nets || !c->finalized[net]) return INET_ERR_STATE;
+    const inethost::NormalForm& nf = c->results[net];
+    if (agents) *agents = nf.agent_data();
+    if (n_agents) *n_agents = nf.n_agents();
+    if (iface) *iface = nf.iface.data();
+    if (n_iface) *n_iface = static_cast<uint32_t>(nf.iface.size());
+    if (eqs) *eqs = nf.eqs.data();
+    if (n_eqs) *n_eqs = static_cast<uint32_t>(nf.eqs.size() / 2);
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 }  // extern "C"

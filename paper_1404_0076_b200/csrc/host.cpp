@@ -14,6 +14,7 @@
 // found in and containers are merged with union-find when a term is spliced,
 // so the test is O(alpha) instead of O(term size) and the whole pass is linear
 // even for an 8,190-deep Ackermann(3,10) result chain in any order.
+#include <new>
 #include "host.h"
 
 #include <algorithm>
@@ -552,17 +553,29 @@ int copy_text(const std::string& s, char* buf, size_t cap, size_t* len) {
 
 extern "C" int inet_finalize_flat(uint32_t* agents, uint32_t n_agents, uint32_t* iface, uint32_t n_iface,
                                   uint32_t* eqs, uint32_t n_eqs, uint32_t n_vars, uint8_t* alive) {
-  if ((n_agents && !agents) || (n_iface && !iface) || (n_eqs && !eqs)) return INET_ERR_ARG;
-  return inethost::finalize_flat(agents, n_agents, iface, n_iface, eqs, n_eqs, n_vars, alive);
+  try {
+    if ((n_agents && !agents) || (n_iface && !iface) || (n_eqs && !eqs)) return INET_ERR_ARG;
+    return inethost::finalize_flat(agents, n_agents, iface, n_iface, eqs, n_eqs, n_vars, alive);
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
 }
 
 extern "C" int inet_print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface, uint32_t n_iface,
                                const uint32_t* eqs, uint32_t n_eqs, const char* const* names, const uint8_t* arity,
                                uint32_t n_labels, char* buf, size_t cap, size_t* len) {
-  if ((n_agents && !agents) || (n_iface && !iface) || (n_eqs && !eqs) || (n_labels && (!names || !arity)) || !len)
+  try {
+    if ((n_agents && !agents) || (n_iface && !iface) || (n_eqs && !eqs) || (n_labels && (!names || !arity)) || !len)
+      return INET_ERR_ARG;
+    std::string text;
+    const int st = inethost::print_flat(agents, n_agents, iface, n_iface, eqs, n_eqs, names, arity, n_labels, text);
+    if (st) return st;
+    return inethost::copy_text(text, buf, cap, len);
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
     return INET_ERR_ARG;
-  std::string text;
-  const int st = inethost::print_flat(agents, n_agents, iface, n_iface, eqs, n_eqs, names, arity, n_labels, text);
-  if (st) return st;
-  return inethost::copy_text(text, buf, cap, len);
+  }
 }

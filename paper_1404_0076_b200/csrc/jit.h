@@ -17,5 +17,7 @@ std::string kernel_source(const uint32_t* blob, size_t n_words, int tier, uint32
 bool available();
 // Compile (or fetch from the on-disk cache) to an sm_100a cubin; 0 on success.
 int compile_cubin(const std::string& source, std::vector<char>& cubin, std::string& log);
+// Compile into the package's kernels/ directory (build time), skipping caches.
+int precompile(const std::string& source, std::string& log);
 
 }  // namespace inetjit

@@ -53,20 +53,31 @@ class Labels:
         self.symbols.append(sym)
         return self.index[sym.name]
 
+    def add_tree(self, term) -> None:
+        """Number every symbol occurring in ``term``."""
+        work = [term]
+        while work:
+            x = work.pop()
+            if not is_var(x):
+                if x.sym.name not in self.index:
+                    self.add(x.sym)
+                work.extend(x.children)
+
     @classmethod
     def of(cls, rules, configs=()) -> "Labels":
+        """Declared symbols first (declaration order), then symbols that only
+        occur on some rule's right-hand side (a RuleSet built in code declares
+        only the pattern symbols, core.py:232-239), then those of the nets."""
         lab = cls()
         for s in rules.symbols.values():
             lab.add(s)
+        for rule in rules.rules.values():
+            for e in rule.rhs:
+                lab.add_tree(e.lhs)
+                lab.add_tree(e.rhs)
         for cfg in configs:
             for t in _roots(cfg):
-                work = [t]
-                while work:
-                    x = work.pop()
-                    if not is_var(x):
-                        if x.sym.name not in lab.index:
-                            lab.add(x.sym)
-                        work.extend(x.children)
+                lab.add_tree(t)
         return lab
 
 
@@ -77,17 +88,66 @@ def _roots(cfg):
         yield e.rhs
 
 
+def _term_key(t, ren):
+    """Hashable skeleton of a rule term; variables through ``ren``."""
+    if is_var(t):
+        return (("v", ren(t.id)),)
+    out = []
+    work = [t]
+    while work:  # preorder, iterative
+        x = work.pop()
+        if is_var(x):
+            out.append(("v", ren(x.id)))
+        else:
+            out.append((x.sym.name, len(x.children)))
+            work.extend(reversed(x.children))
+    return tuple(out)
+
+
+def same_symbol_rule_is_symmetric(rule) -> bool:
+    """True if ``A(x..) >< A(y..) => rhs`` is unchanged when the two pattern
+    agents trade places (x_k <-> y_k), up to renaming its bound variables and
+    the order/orientation of its equations.
+
+    The reference applies a same-symbol rule in the active equation's own
+    orientation (core.py:287-298). The device forms an active pair by a merge
+    in arrival order, so only rules whose result does not depend on the
+    orientation are accepted (``UnsupportedNet`` otherwise)."""
+    swap = dict(zip(rule.a_vars, rule.b_vars))
+    swap.update(zip(rule.b_vars, rule.a_vars))
+    bound = list(rule.bound_vars)
+
+    def eq_multiset(ren):
+        return sorted(tuple(sorted((_term_key(e.lhs, ren), _term_key(e.rhs, ren)))) for e in rule.rhs)
+
+    want = eq_multiset(lambda v: v)
+    # try every renaming of the bound variables (a rule has at most 8; same-symbol
+    # rules in practice 0-2, so this is a handful of comparisons)
+    import itertools
+
+    for perm in itertools.permutations(bound):
+        m = dict(zip(bound, perm))
+        if eq_multiset(lambda v: swap[v] if v in swap else m[v]) == want:
+            return True
+    return False
+
+
 def compile_rules(rules, labels: Labels) -> np.ndarray:
     """RuleSet -> uint32 rule blob (layout in include/inet_b200.h)."""
     L = len(labels.symbols)
     rule_list = list(rules.rules.values())
     if len(rule_list) > MAX_RULES:
         raise UnsupportedNet(f"more than {MAX_RULES} rules")
+    for rule in rule_list:
+        if rule.lhs_a.name == rule.lhs_b.name and not same_symbol_rule_is_symmetric(rule):
+            raise UnsupportedNet(
+                f"rule {rule.lhs_a.name}><{rule.lhs_b.name} is not symmetric in its two agents: its result "
+                "would depend on the orientation of a pair formed by communication")
     pair = np.full(L * L + (L * L) % 2, 0xFFFF, dtype=np.uint16)
     recs = np.zeros((len(rule_list), 16), dtype=np.uint32)
     for ri, rule in enumerate(rule_list):
-        la = labels.index[rule.lhs_a.name]
-        lb = labels.index[rule.lhs_b.name]
+        la = labels.add(rule.lhs_a)
+        lb = labels.add(rule.lhs_b)
         pair[la * L + lb] = ri << 1
         if la != lb:
             pair[lb * L + la] = (ri << 1) | 1
@@ -109,7 +169,7 @@ def compile_rules(rules, labels: Labels) -> np.ndarray:
             slot = len(new_agents)
             if slot >= MAX_NEW:
                 raise UnsupportedNet(f"rule {rule.lhs_a.name}><{rule.lhs_b.name}: too many rhs agents")
-            rec = [labels.index[term.sym.name], SRC_NONE, SRC_NONE, SRC_NONE]
+            rec = [labels.add(term.sym), SRC_NONE, SRC_NONE, SRC_NONE]
             new_agents.append(rec)
             work = [(term, rec)]
             while work:
@@ -122,7 +182,7 @@ def compile_rules(rules, labels: Labels) -> np.ndarray:
                         if s >= MAX_NEW:
                             raise UnsupportedNet(
                                 f"rule {rule.lhs_a.name}><{rule.lhs_b.name}: too many rhs agents")
-                        cr = [labels.index[ch.sym.name], SRC_NONE, SRC_NONE, SRC_NONE]
+                        cr = [labels.add(ch.sym), SRC_NONE, SRC_NONE, SRC_NONE]
                         new_agents.append(cr)
                         r[1 + k] = SRC_NEW + s
                         work.append((ch, cr))
@@ -193,13 +253,21 @@ def flatten(config, labels: Labels) -> FlatNet:
     iface = [ref(t) for t in config.interface]
     eqs = [(ref(e.lhs), ref(e.rhs)) for e in config.equations]
     max_id = max(var_ids) if var_ids else -1
-    return FlatNet(
-        agents=np.array(agents, dtype=np.uint32).reshape(-1, 4),
-        eqs=np.array(eqs, dtype=np.uint32).reshape(-1, 2),
-        iface=np.array(iface, dtype=np.uint32),
-        var_ids=var_ids,
-        fresh_base=max_id + 1,
-    )
+    ag = np.array(agents, dtype=np.uint32).reshape(-1, 4)
+    eq = np.array(eqs, dtype=np.uint32).reshape(-1, 2)
+    fc = np.array(iface, dtype=np.uint32)
+    # dense ids in the order of the original ids: the device compares input
+    # variables by id where the reference keys var = var on the smaller id
+    # (engine.py:150-153)
+    if any(var_ids[i] > var_ids[i + 1] for i in range(len(var_ids) - 1)):
+        order = np.argsort(np.asarray(var_ids, dtype=np.int64), kind="stable")
+        rank = np.empty(len(var_ids), dtype=np.uint32)
+        rank[order] = np.arange(len(var_ids), dtype=np.uint32)
+        for arr in (ag, eq, fc):
+            m = (arr != NONE) & ((arr & VAR) != 0)
+            arr[m] = VAR | rank[arr[m] & ~np.uint32(VAR)]
+        var_ids = [var_ids[i] for i in order]
+    return FlatNet(agents=ag, eqs=eq, iface=fc, var_ids=var_ids, fresh_base=max_id + 1)
 
 
 def term_classes(config):

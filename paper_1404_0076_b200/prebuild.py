@@ -1,0 +1,62 @@
+"""Build step: precompile the rule-set kernels of the shipped programs.
+
+The first ``evaluate()`` of a rule set otherwise runs NVRTC (0.7-1.1 s per
+kernel variant). ``precompile_shipped()`` compiles, for the benchmark
+programs (the reference's programs/*.inet), every variant the engine picks
+for them — tier S batches at 128/256/512 threads, tier M single nets, the
+16-CTA cluster (tier C), the whole-GPU tier X; with and without the
+reference-loop code; the per-rule counters where bench.py asks for them —
+into ``kernels/`` next to libinetb200.so, where every later process finds
+them (jit.cpp ``package_dir``). Runs on the build host; no GPU needed.
+"""
+
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+
+from . import _native
+from .engine import prepare
+from .programs import load_rules, program
+
+# (tier, threads) the engine's tier selection uses (engine.cu auto_threads /
+# cluster_threads): batches of >= 1024, >= 256, >= 16 nets; single nets.
+VARIANTS = [
+    (_native.TIER_S, 128), (_native.TIER_S, 256), (_native.TIER_S, 512),
+    (_native.TIER_M, 256), (_native.TIER_C, 256), (_native.TIER_X, 256),
+]
+
+
+def shipped_blobs() -> dict:
+    """Rule blob of every shipped program, numbered as evaluate() numbers it."""
+    out = {}
+    for name in ("addition", "ackermann", "fibonacci", "lsystem"):
+        p = program(name)
+        out[name] = prepare([p.build_input(*p.default_params)], p.rules).blob
+    out["arith"] = prepare([], load_rules("arith")).blob
+    return out
+
+
+def precompile_shipped(workers: int = 8) -> list:
+    jobs = []
+    for name, blob in shipped_blobs().items():
+        for tier, threads in VARIANTS:
+            for exact in (False, True):
+                jobs.append((name, blob, tier, threads, exact, False))
+        # accounting runs of bench.py (per-rule histogram)
+        if name in ("ackermann", "lsystem", "fibonacci"):
+            for tier, threads in ((_native.TIER_S, 128), (_native.TIER_M, 256), (_native.TIER_C, 256),
+                                  (_native.TIER_X, 256)):
+                jobs.append((name, blob, tier, threads, False, True))
+    failed = []
+
+    def one(job):
+        name, blob, tier, threads, exact, count = job
+        code, log = _native.jit_precompile(blob, tier, threads, exact, count)
+        if code != 0:
+            failed.append((name, tier, threads, exact, count, log[-400:]))
+
+    with ThreadPoolExecutor(workers) as ex:
+        list(ex.map(one, jobs))
+    if failed:
+        raise RuntimeError(f"precompile failed: {failed}")
+    return jobs
