@@ -33,6 +33,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the reference package `inet` (net builders, value oracles) from baseline/_ref
+sys.path.append(os.path.join(ROOT, "baseline", "_ref"))
 
 BATCH_NETS = 4096
 BATCH_PARAMS = (3, 6)
@@ -171,7 +173,7 @@ class ClockSampler:
 
 
 def rule_bytes(rules) -> list[int]:
-    from paper_1404_0076_b200.core import is_var
+    from paper_1404_0076_b200.flat import is_var
 
     out = []
     for rule in rules.rules.values():
@@ -218,7 +220,7 @@ def ncu_traffic(workload: str):
 def cpu_sample(program_name: str, params, seconds: float, threads: int) -> dict:
     """Time the oracle (reference algorithm, C++ port) on the host for ~seconds."""
     from oracle import oracle as O
-    from paper_1404_0076_b200.programs import program
+    from inet.bench import program
 
     prog = program(program_name)
     rules = O.rules_for(program_name)
@@ -308,7 +310,7 @@ def run_ours(args) -> None:
     import torch.distributed as dist
 
     from paper_1404_0076_b200 import EngineConfig, _native, engine, shard
-    from paper_1404_0076_b200.programs import ackermann_value, fibonacci_value, program
+    from inet.bench import ackermann_value, fibonacci_value, program
 
     rank, local, world = dist_env()
     if world > 1:
@@ -403,7 +405,7 @@ def run_ours(args) -> None:
             "scaling": "strong" if args.workload == "batch" else "replicas",
             "vs_baseline": None,
             "dtype": "u32",
-            "data": "synthetic (deterministic Ackermann nets built by paper_1404_0076_b200.programs, no RNG)",
+            "data": "synthetic (deterministic Ackermann nets built by the reference builders inet.bench.program, no RNG)",
             "config": dict(wl, parallelism=f"dp{world} (nets sharded, no collective)",
                            interactions_per_net=per_net, rounds_per_net=max_rounds,
                            threads_per_net=engine.native_cfg(ecfg).threads or "auto",

@@ -1,26 +1,17 @@
 """B200-native interaction-net evaluator: drop-in for ``inet.engine.evaluate``.
 
-The public surface mirrors the reference package ``inet`` (src/inet/__init__.py)
-for the reduction path: the calculus types, the ``.inet`` parser and canonical
-printer, ``EngineConfig``/``EvalResult``/``LoopStats`` and ``evaluate`` — plus
-``evaluate_batch`` / ``evaluate_sharded`` for many independent nets. The
-reduction itself runs in hand-written CUDA for sm_100a behind the C ABI in
-include/inet_b200.h (``libinetb200.so``, built in-tree).
+The reduction loop (src/inet/engine.py:186-228) runs in hand-written CUDA for
+sm_100a behind the C ABI in include/inet_b200.h (``libinetb200.so``, built
+in-tree). Everything around it is the reference package's own code, imported
+(``_ref``): the calculus types, parser and printer, ``LoopStats`` and the
+exception classes. This package adds ``evaluate`` (same signature and result
+type as the reference's), ``evaluate_batch`` / ``evaluate_sharded`` /
+``evaluate_text`` for many nets and large normal forms, and ``install()``.
 """
 
-from .core import (
-    Agent,
-    Configuration,
-    EqClass,
-    Equation,
-    FreshIdAllocator,
-    Rule,
-    RuleSet,
-    Symbol,
-    Var,
-    classify,
-    find_rule,
-)
+from ._ref import core as _core
+from ._ref import lang as _lang
+from ._ref import profile as _profile
 from .engine import (
     BatchResult,
     EngineConfig,
@@ -33,55 +24,51 @@ from .engine import (
     finalize,
     reduce_by_key,
 )
-from .lang import parse_program, parse_rules, print_configuration, print_program, print_rule
-from .profile import LoopStats, RunProfile, record
+
+Agent, Configuration, Equation, Rule, RuleSet, Symbol, Var = (
+    _core.Agent, _core.Configuration, _core.Equation, _core.Rule, _core.RuleSet, _core.Symbol, _core.Var)
+parse_program, print_configuration = _lang.parse_program, _lang.print_configuration
+LoopStats = _profile.LoopStats
 
 __all__ = [
     "Agent",
     "BatchResult",
     "Configuration",
     "EngineConfig",
-    "EqClass",
     "Equation",
     "EvalResult",
-    "FreshIdAllocator",
     "LoopStats",
     "Rule",
     "RuleSet",
-    "RunProfile",
     "Symbol",
     "Var",
     "check_name_discipline",
-    "classify",
     "evaluate",
     "evaluate_batch",
     "evaluate_sharded",
     "evaluate_text",
     "finalize",
-    "find_rule",
+    "install",
     "parse_program",
-    "parse_rules",
     "print_configuration",
-    "print_program",
-    "print_rule",
-    "record",
     "reduce_by_key",
 ]
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 
 def install(module=None) -> None:
     """Rebind the reference's ``evaluate`` to this engine.
 
     ``install()`` patches ``inet.engine.evaluate`` and ``inet.evaluate`` (and
-    ``inet.cli``'s imported name) so existing callers of the reference —
-    its CLI, bench and tests — run on the GPU without edits. Objects of the
-    reference's own classes go in and come out.
+    the names ``inet.cli`` / ``inet.bench`` imported) so existing callers of
+    the reference — its CLI, bench and tests — run on the GPU without edits.
     """
     import importlib
 
-    ref = module or importlib.import_module("inet")
+    from . import _ref
+
+    ref = module or _ref.inet
     ref_engine = importlib.import_module(ref.__name__ + ".engine")
     ref_engine.evaluate = evaluate
     ref.evaluate = evaluate

@@ -18,7 +18,6 @@ calls raise ``DeviceError``.
 
 from __future__ import annotations
 
-import importlib
 import threading
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence, TypeVar
@@ -26,7 +25,9 @@ from typing import Callable, Optional, Sequence, TypeVar
 import numpy as np
 
 from . import _native
-from .core import Configuration, Equation, RuleSet, Term, is_var, iter_vars
+from ._ref import core as _core
+from ._ref import engine as _ref_engine
+from ._ref import profile as _profile
 from .errors import (
     ArenaExhausted,
     DeviceError,
@@ -35,41 +36,44 @@ from .errors import (
     NoRuleForPair,
     SlotOverflow,
 )
-from .flat import FlatNet, Labels, compile_rules, flatten, term_classes, unflatten
-from .profile import LoopStats
+from .flat import FlatNet, Labels, compile_rules, flatten, is_var, term_classes, unflatten
+
+Configuration, Equation, RuleSet, Term = _core.Configuration, _core.Equation, _core.RuleSet, _core.Term
+iter_vars = _core.iter_vars
+LoopStats = _profile.LoopStats
+EvalResult = _ref_engine.EvalResult
 
 T = TypeVar("T")
 
 
 @dataclass(slots=True)
-class EngineConfig:
-    """Same fields and defaults as the reference (engine.py:35-48).
+class EngineConfig(_ref_engine.EngineConfig):
+    """The reference's ``EngineConfig`` (engine.py:35-48) plus device knobs.
 
-    ``worker_hint`` is accepted for compatibility; the device decides its own
-    parallelism. ``device`` selects the GPU; ``threads`` the CTA size per net
-    (0 = auto); ``ctas_per_net`` the cluster size of a single net (0 = auto);
-    ``exact_loops`` keeps the reference's loop structure (a merged equation
-    that is still var-headed communicates in the next loop, so ``loops`` rows
-    are the reference's), False links to a fixpoint within a round.
+    The reference's own ``EngineConfig`` is accepted everywhere (the extra
+    fields then take their defaults). ``worker_hint`` is accepted for
+    compatibility; the device decides its own parallelism. ``device`` selects
+    the GPU; ``threads`` the CTA size per net (0 = auto); ``ctas_per_net`` the
+    cluster size of a single net (0 = auto); ``exact_loops`` keeps the
+    reference's loop structure (a merged equation that is still var-headed
+    communicates in the next loop, so ``loops`` rows are the reference's),
+    False links to a fixpoint within a round.
     """
 
-    slot_count: Optional[int] = None
-    max_loops: int = 1_000_000
-    worker_hint: int = 1
-    collect_stats: bool = True
-    validate_phases: bool = False
     device: int = 0
     threads: int = 0
     ctas_per_net: int = 0
     exact_loops: bool = True
 
 
-@dataclass(slots=True)
-class EvalResult:
-    final: Configuration
-    loops: list[LoopStats]
-    total_interactions: int
-    total_communications: int
+def as_engine_config(cfg) -> EngineConfig:
+    """A copy of ``cfg`` (this package's or the reference's ``EngineConfig``) as an ``EngineConfig``."""
+    out = EngineConfig()
+    for cls in type(cfg).__mro__:
+        for f in getattr(cls, "__slots__", ()):
+            if hasattr(cfg, f):
+                setattr(out, f, getattr(cfg, f))
+    return out
 
 
 def reduce_by_key(items: Sequence[T], key: Callable[[T], object], merge: Callable[[T, T], T]) -> list[T]:
@@ -106,54 +110,18 @@ def check_name_discipline(interface: Sequence[Term], eqs: Sequence[Equation]) ->
 # error mapping
 
 
-def _errors_for(config):
-    """The caller's errors module (reference objects get reference exceptions)."""
-    mod = type(config).__module__
-    pkg = mod.rsplit(".", 1)[0] if "." in mod else None
-    if pkg and pkg != __name__.rsplit(".", 1)[0]:
-        try:
-            return importlib.import_module(pkg + ".errors")
-        except ImportError:
-            pass
-    from . import errors
-
-    return errors
-
-
-def _raise_status(code: int, st, labels: Labels, cfg: EngineConfig, errs) -> None:
+def _raise_status(code: int, st, labels: Labels, cfg: EngineConfig) -> None:
     if code == _native.NO_RULE:
         a = labels.symbols[st.err_label_a].name
         b = labels.symbols[st.err_label_b].name
-        raise getattr(errs, "NoRuleForPair", NoRuleForPair)(a, b)
+        raise NoRuleForPair(a, b)
     if code == _native.LOOP_CAP:
-        raise getattr(errs, "LoopCapExceeded", LoopCapExceeded)(cfg.max_loops)
+        raise LoopCapExceeded(cfg.max_loops)
     if code == _native.ARENA:
         raise ArenaExhausted(
             f"device arena exhausted at {st.cap_agents} agents / {st.cap_vars} variables per net"
         )
     raise DeviceError(code, _native.strerror(code))
-
-
-def _loop_stats_class(config):
-    mod = type(config).__module__
-    pkg = mod.rsplit(".", 1)[0] if "." in mod else None
-    if pkg and pkg != __name__.rsplit(".", 1)[0]:
-        try:
-            return importlib.import_module(pkg + ".profile").LoopStats
-        except (ImportError, AttributeError):
-            pass
-    return LoopStats
-
-
-def _result_class(config):
-    mod = type(config).__module__
-    pkg = mod.rsplit(".", 1)[0] if "." in mod else None
-    if pkg and pkg != __name__.rsplit(".", 1)[0]:
-        try:
-            return importlib.import_module(pkg + ".engine").EvalResult
-        except (ImportError, AttributeError):
-            pass
-    return EvalResult
 
 
 # ---------------------------------------------------------------------------
@@ -202,9 +170,9 @@ def native_cfg(cfg: EngineConfig) -> _native.Cfg:
     k = _native.Cfg()
     k.max_loops = max(0, min(int(cfg.max_loops), 0xFFFFFFFE))
     k.collect_stats = 1 if cfg.collect_stats else 0
-    k.threads = cfg.threads
-    k.ctas_per_net = cfg.ctas_per_net
-    k.exact_loops = 1 if cfg.exact_loops else 0
+    k.threads = getattr(cfg, "threads", 0)
+    k.ctas_per_net = getattr(cfg, "ctas_per_net", 0)
+    k.exact_loops = 1 if getattr(cfg, "exact_loops", True) else 0
     return k
 
 
@@ -217,9 +185,8 @@ def run_prepared(ctx: _native.Context, prep: Prepared, cfg: EngineConfig) -> tup
 def evaluate(config: Configuration, rules: RuleSet, cfg: Optional[EngineConfig] = None) -> EvalResult:
     """Reduce ``config`` to normal form on the GPU (engine.py:186-228)."""
     cfg = cfg if cfg is not None else EngineConfig()
-    errs = _errors_for(config)
     if cfg.slot_count is not None and cfg.slot_count < rules.max_rhs_size:
-        raise getattr(errs, "SlotOverflow", SlotOverflow)(
+        raise SlotOverflow(
             f"slot_count {cfg.slot_count} is smaller than the largest rule rhs ({rules.max_rhs_size})"
         )
     if cfg.validate_phases:
@@ -230,7 +197,7 @@ def evaluate(config: Configuration, rules: RuleSet, cfg: Optional[EngineConfig] 
         code, _ms = run_prepared(ctx, prep, cfg)
         st = ctx.stats(0)
         if code != _native.OK:
-            _raise_status(code, st, prep.labels, cfg, errs)
+            _raise_status(code, st, prep.labels, cfg)
         ctx.finalize(0, 1)
         agents, iface, eqs = ctx.result(0)
         rows = ctx.rounds(0) if cfg.collect_stats else None
@@ -239,9 +206,8 @@ def evaluate(config: Configuration, rules: RuleSet, cfg: Optional[EngineConfig] 
         check_name_discipline(final.interface, final.equations)
     loops = []
     if rows is not None:
-        LS = _loop_stats_class(config)
-        loops = [LS(i + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for i, r in enumerate(rows)]
-    return _result_class(config)(final, loops, int(st.interactions), int(st.communications))
+        loops = [LoopStats(i + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for i, r in enumerate(rows)]
+    return EvalResult(final, loops, int(st.interactions), int(st.communications))
 
 
 @dataclass
@@ -295,9 +261,8 @@ def evaluate_batch(
     cfg = cfg if cfg is not None else EngineConfig(collect_stats=False)
     if not configs:
         return BatchResult([], 0.0, 0, 0, 0)
-    errs = _errors_for(configs[0])
     if cfg.slot_count is not None and cfg.slot_count < rules.max_rhs_size:
-        raise getattr(errs, "SlotOverflow", SlotOverflow)(
+        raise SlotOverflow(
             f"slot_count {cfg.slot_count} is smaller than the largest rule rhs ({rules.max_rhs_size})"
         )
     ctx = _native.context(getattr(cfg, "device", 0))
@@ -308,7 +273,7 @@ def evaluate_batch(
             for i in range(len(configs)):
                 st = ctx.stats(i)
                 if st.status != _native.OK:
-                    _raise_status(st.status, st, prep.labels, cfg, errs)
+                    _raise_status(st.status, st, prep.labels, cfg)
         ti, tc, mr, _nf = ctx.totals()
         stats = [ctx.stats(i) for i in range(len(configs))]
         finals = [None] * len(configs)
@@ -325,16 +290,14 @@ def evaluate_batch(
         if cfg.collect_stats:
             rows = [ctx.rounds(i) for i in range(len(configs))]
     out = []
-    LS = _loop_stats_class(configs[0])
-    ER = _result_class(configs[0])
     for i, c in enumerate(configs):
         final = None
         if finals[i] is not None:
             final = unflatten(*finals[i], prep.labels, prep.flats[i], term_classes(c))
         loops = []
         if rows[i] is not None:
-            loops = [LS(j + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for j, r in enumerate(rows[i])]
-        out.append(ER(final, loops, int(stats[i].interactions), int(stats[i].communications)))
+            loops = [LoopStats(j + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for j, r in enumerate(rows[i])]
+        out.append(EvalResult(final, loops, int(stats[i].interactions), int(stats[i].communications)))
     return BatchResult(out, ms, ti, tc, mr, texts)
 
 
@@ -360,10 +323,8 @@ def evaluate_sharded(
 
     def work(k: int) -> None:
         try:
-            import dataclasses
-
-            base = cfg if cfg is not None else EngineConfig(collect_stats=False)
-            c = dataclasses.replace(base, device=devices[k])
+            c = as_engine_config(cfg if cfg is not None else EngineConfig(collect_stats=False))
+            c.device = devices[k]
             parts[k] = evaluate_batch(configs[bounds[k] : bounds[k + 1]], rules, c, as_terms)
         except BaseException as exc:  # surfaced below
             errors.append(exc)
@@ -387,15 +348,8 @@ def evaluate_sharded(
 
 def finalize(eqs: Sequence[Equation], interface: Sequence[Term]) -> Configuration:
     """Sequential cleanup (engine.py:287-362) via the native host routine."""
-    from .core import Var as _V
-
-    probe = next(iter(list(interface) + [e.lhs for e in eqs]), None)
     cfg = Configuration(tuple(interface), tuple(eqs))
     classes = term_classes(cfg)
-    if probe is not None:
-        mod = importlib.import_module(type(probe).__module__)
-        if all(hasattr(mod, n) for n in ("Var", "Agent", "Equation", "Configuration")):
-            classes = (mod.Var, mod.Agent, mod.Equation, mod.Configuration)
     labels = Labels()
     flat = flatten(cfg, labels)
     agents, iface, feqs, alive = _native.finalize_flat(
@@ -427,7 +381,6 @@ def finalize(eqs: Sequence[Equation], interface: Sequence[Term]) -> Configuratio
                         work.append((p, False))
         return out[r]
 
-    _ = _V
     return Configuration_(
         tuple(build(int(r)) for r in iface),
         tuple(Equation_(build(int(l)), build(int(rr))) for (l, rr), ok in zip(feqs.reshape(-1, 2), alive) if ok),

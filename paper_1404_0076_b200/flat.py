@@ -1,7 +1,7 @@
 """Host <-> device formats: rule-table compiler and net flattener.
 
 ``compile_rules`` turns a ``RuleSet`` (the reference's Rule/RuleSet,
-core.py:158-251, or this package's mirror) into the rule blob documented in
+core.py:158-251) into the rule blob documented in
 include/inet_b200.h: a dense ``[label][label] -> (rule, swap)`` table plus one
 16-word record per rule listing its new agents and right-hand-side equations
 as *sources* (port k of either pattern agent, fresh variable j, new agent m).
@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .core import is_var
+from ._ref import core as _core
 from .errors import UnsupportedNet
 
 NONE = 0xFFFFFFFF
@@ -30,6 +30,11 @@ MAGIC = 0x31524E49
 MAX_ARITY, MAX_LABELS, MAX_RULES = 3, 64, 256
 MAX_NEW, MAX_EQ, MAX_FRESH = 8, 8, 8
 SRC_FRESH, SRC_NEW, SRC_NONE = 6, 14, 22
+
+
+def is_var(t) -> bool:
+    """Variable test on the reference's terms (core.py:33-62): agents carry ``sym``."""
+    return not hasattr(t, "sym")
 
 
 @dataclass
@@ -275,9 +280,7 @@ def term_classes(config):
     mod = sys.modules.get(type(config).__module__)
     if mod is not None and all(hasattr(mod, n) for n in ("Var", "Agent", "Equation", "Configuration")):
         return mod.Var, mod.Agent, mod.Equation, mod.Configuration
-    from . import core
-
-    return core.Var, core.Agent, core.Equation, core.Configuration
+    return _core.Var, _core.Agent, _core.Equation, _core.Configuration
 
 
 def unflatten(agents: np.ndarray, iface: np.ndarray, eqs: np.ndarray, labels: Labels, flat: FlatNet,

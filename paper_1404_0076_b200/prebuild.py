@@ -16,7 +16,9 @@ from concurrent.futures import ThreadPoolExecutor
 
 from . import _native
 from .engine import prepare
-from .programs import load_rules, program
+from ._ref import bench as _bench
+
+load_rules, program = _bench.load_rules, _bench.program
 
 # (tier, threads) the engine's tier selection uses (engine.cu auto_threads /
 # cluster_threads): batches of >= 1024, >= 256, >= 16 nets; single nets.

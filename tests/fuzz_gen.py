@@ -8,7 +8,7 @@ the result not to depend on the pair's orientation). Nets obey the name
 discipline (every variable occurs exactly twice).
 """
 
-from paper_1404_0076_b200.core import Agent, Configuration, Equation, Rule, RuleSet, Symbol, Var
+from inet.core import Agent, Configuration, Equation, Rule, RuleSet, Symbol, Var
 
 
 def random_signature(rng, n=None):

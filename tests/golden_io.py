@@ -13,7 +13,7 @@ def load(name):
 
 def to_config(net, symbols_cls=None):
     """Golden flat net -> this repo's Configuration (original variable ids)."""
-    from paper_1404_0076_b200.core import Agent, Configuration, Equation, Symbol, Var
+    from inet.core import Agent, Configuration, Equation, Symbol, Var
 
     syms = [Symbol(n, a) for n, a in net["symbols"]]
     recs = net["agents"]
@@ -29,7 +29,7 @@ def to_config(net, symbols_cls=None):
 
 def to_rules(rs):
     """Golden flat rule set -> this repo's RuleSet."""
-    from paper_1404_0076_b200.core import Agent, Equation, Rule, RuleSet, Symbol, Var
+    from inet.core import Agent, Equation, Rule, RuleSet, Symbol, Var
 
     syms = {n: Symbol(n, a) for n, a in rs["symbols"]}
     names = [n for n, _ in rs["symbols"]]

@@ -89,7 +89,7 @@ def test_random_rule_sets_single_net_tiers(seed, ctas):
 def test_netgraph_canonical_form():
     """The comparison itself: invariant under equation order and orientation,
     sensitive to a changed agent or a rewired port."""
-    from paper_1404_0076_b200.core import Agent, Configuration, Equation, Symbol, Var
+    from inet.core import Agent, Configuration, Equation, Symbol, Var
 
     rng = random.Random(4)
     rules, nets = _case(0, 60)

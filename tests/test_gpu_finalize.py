@@ -10,7 +10,7 @@ import pytest
 
 from oracle import oracle as O
 from paper_1404_0076_b200 import EngineConfig, _native, engine, print_configuration
-from paper_1404_0076_b200 import programs
+from paper_1404_0076_b200._ref import bench as programs
 from paper_1404_0076_b200.flat import unflatten
 
 from test_gpu_parity import _random_arith_net

@@ -23,7 +23,8 @@ from paper_1404_0076_b200 import (
     parse_program,
     print_configuration,
 )
-from paper_1404_0076_b200 import errors, programs
+from paper_1404_0076_b200 import errors
+from paper_1404_0076_b200._ref import bench as programs
 
 pytestmark = pytest.mark.gpu
 

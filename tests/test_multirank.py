@@ -28,7 +28,7 @@ def _worker(rank, world, port, n_nets, out):
 
     from oracle import oracle as O
     from paper_1404_0076_b200 import shard
-    from paper_1404_0076_b200.programs import program
+    from inet.bench import program
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -80,7 +80,7 @@ def test_two_rank_gloo_shard_and_gather():
     assert t == 2.0  # max over ranks
     assert tot[1] == n_nets
     assert [(m, n) for m, n, _, _ in allv] == [(2, k % 4) for k in range(n_nets)]
-    from paper_1404_0076_b200.programs import ackermann_value
+    from inet.bench import ackermann_value
 
     for m, n, ints, text in allv:
         assert text.count("S(") == ackermann_value(m, n)

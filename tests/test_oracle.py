@@ -62,7 +62,7 @@ def test_oracle_matches_reference_on_551_arith_nets():
 
 def test_survey_goldens_ackermann_3_7_and_3_8():
     """Totals measured on the reference in SURVEY.md §8(c) / Appendix A."""
-    from paper_1404_0076_b200.programs import program
+    from inet.bench import program
 
     prog = program("ackermann")
     rules = O.rules_for("ackermann")
@@ -77,7 +77,7 @@ def test_survey_goldens_ackermann_3_7_and_3_8():
 
 def test_closed_form_interactions_for_ackermann_3_n():
     """I(n) = (256*4^n + 50)/3 - 72*2^n + 5n, L(n) = 56*2^n - 8n - 37."""
-    from paper_1404_0076_b200.programs import program
+    from inet.bench import program
 
     prog = program("ackermann")
     rules = O.rules_for("ackermann")

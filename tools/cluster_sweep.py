@@ -6,7 +6,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1404_0076_b200 import EngineConfig, _native, engine, evaluate, print_configuration  # noqa: E402
-from paper_1404_0076_b200.programs import program  # noqa: E402
+from inet.bench import program  # noqa: E402
 
 WL = {"a23": ("ackermann", (2, 3), 90, "829772e6f0876f88"), "fib18": ("fibonacci", (18,), 50515, "0feb32862e23b545"),
       "a36": ("ackermann", (3, 6), 344964, "47b60c6a324411a9"), "a38": ("ackermann", (3, 8), 5574030, "b85606c71178de4b"),

@@ -9,7 +9,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1404_0076_b200 import EngineConfig, _native, engine  # noqa: E402
-from paper_1404_0076_b200.programs import program  # noqa: E402
+from inet.bench import program  # noqa: E402
 
 spec = {"a23": ("ackermann", (2, 3)), "a38": ("ackermann", (3, 8)), "a310": ("ackermann", (3, 10)),
         "fib18": ("fibonacci", (18,)), "a36": ("ackermann", (3, 6))}[sys.argv[1]]

@@ -1,7 +1,7 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1404_0076_b200 import EngineConfig, evaluate, errors
-from paper_1404_0076_b200.programs import program
+from inet.bench import program
 p = program("ackermann")
 for g in (0, 2):
     try:

@@ -2,7 +2,7 @@
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1404_0076_b200 import EngineConfig, _native, engine  # noqa: E402
-from paper_1404_0076_b200.programs import program  # noqa: E402
+from inet.bench import program  # noqa: E402
 p = program("ackermann")
 prep = engine.prepare([p.build_input(3, 6) for _ in range(4096)], p.rules)
 ctx = _native.Context(0)

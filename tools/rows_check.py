@@ -7,7 +7,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import oracle as O  # noqa: E402
 from paper_1404_0076_b200 import EngineConfig, evaluate, print_configuration  # noqa: E402
-from paper_1404_0076_b200.programs import program  # noqa: E402
+from inet.bench import program  # noqa: E402
 
 p = program("ackermann")
 for n in [int(x) for x in (sys.argv[1:] or ["8", "10"])]:

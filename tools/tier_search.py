@@ -6,7 +6,7 @@ import time
 os.environ.setdefault("INET_B200_DEBUG", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1404_0076_b200 import EngineConfig, evaluate_text  # noqa: E402
-from paper_1404_0076_b200.programs import program  # noqa: E402
+from inet.bench import program  # noqa: E402
 
 for name, params in (("lsystem", (26,)), ("lsystem", (24,)), ("ackermann", (3, 10))):
     p = program(name)

@@ -4,7 +4,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1404_0076_b200 import EngineConfig, _native, engine  # noqa: E402
-from paper_1404_0076_b200.programs import program  # noqa: E402
+from inet.bench import program  # noqa: E402
 
 p = program("lsystem")
 prep = engine.prepare([p.build_input(int(sys.argv[1]) if len(sys.argv) > 1 else 26)], p.rules)
