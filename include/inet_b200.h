@@ -118,7 +118,7 @@ typedef struct inet_net_stats {
   uint32_t jit;            /* 1 if the rule-set specialised kernel ran (else the interpreter) */
   uint32_t sm_mhz;         /* effective SM clock over this net's reduction (clock64 / globaltimer) */
   uint32_t device_final;   /* 1 if the normal form was finalized on the device (tier S), else the host did */
-  uint32_t reserved;
+  uint32_t threads;        /* CTA size (threads per net, per CTA of a cluster) of the kernel that ran */
 } inet_net_stats;
 
 /* Context: one device, one stream, device buffers reused across calls.

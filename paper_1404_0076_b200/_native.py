@@ -77,7 +77,7 @@ class NetStats(C.Structure):
         ("jit", C.c_uint32),
         ("sm_mhz", C.c_uint32),
         ("device_final", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("threads", C.c_uint32),
     ]
 
 

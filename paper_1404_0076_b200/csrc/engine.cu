@@ -217,6 +217,7 @@ struct inet_ctx {
   // rule-set specialised kernels (jit.cpp), keyed by (tier, block size)
   int jit_mode = 1;  // 0 = prebuilt interpreter only
   bool last_jit = false;
+  uint32_t last_threads = 0;  // CTA size of the last launch
   std::string jit_log;
   std::map<std::tuple<int, uint32_t, int>, std::pair<cudaLibrary_t, cudaKernel_t>> jit_kernels;
   int jit_style = -1;  // -1: per tier (measured defaults); env INET_B200_JITSTYLE overrides
@@ -541,6 +542,7 @@ int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
   const void* jk = jit_kernel(c, tier, threads);
   const void* fn = jk ? jk : reinterpret_cast<const void*>(pick_kernel(threads, tier));
   c->last_jit = jk != nullptr;
+  c->last_threads = threads;
   const size_t smem = size_t(plan_smem(sh, tier).words) * 4;
   int dev_sms = 0, max_optin = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -882,6 +884,7 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     s.jit = c->last_jit ? 1u : 0u;
     s.sm_mhz = k.pad[0];
     s.device_final = c->dev_rows[i] ? 1u : 0u;
+    s.threads = c->last_threads;
     if (first == INET_OK && k.err) first = static_cast<int>(k.err);
   }
   c->reduced = true;

@@ -167,6 +167,30 @@ def test_batch_of_ackermann_3_6():
         assert programs.nat_value(r.final.interface[0]) == 509
 
 
+def test_headline_batch_4096_ackermann_3_6():
+    """BASELINE.json configs[4], the kernel variant bench.py times: 4096 x A(3,6) through
+    evaluate_batch with automatic threads (tier S, 128 threads per net, no per-rule
+    counters, normal forms finalized on the device and printed natively). Every
+    net's printed normal form equals the reference's (cases.json, generated by the
+    reference), and the total is SURVEY.md §8(c)'s 1,412,972,544."""
+    from paper_1404_0076_b200 import _native
+
+    case = next(c for c in CASES if c.get("program") == "ackermann" and c["params"] == [3, 6])
+    prog = programs.program("ackermann")
+    nets = [prog.build_input(3, 6) for _ in range(4096)]
+    out = evaluate_batch(nets, prog.rules, EngineConfig(collect_stats=False), as_terms=False, as_text=True)
+    assert out.total_interactions == 1_412_972_544
+    assert out.max_rounds == 3_499  # the reference's loop count (SURVEY.md §8(c))
+    assert len(out.texts) == 4096
+    bad = [i for i, t in enumerate(out.texts) if _sha(t) != case["print_sha256"]]
+    assert not bad, f"{len(bad)} nets differ, first {bad[:5]}"
+    assert all(r.total_interactions == 344_964 for r in out.results)
+    assert all(r.total_communications == case["communications"] for r in out.results)
+    ctx = _native.context(0)
+    st = ctx.stats(4095)
+    assert (st.tier, st.threads, st.jit, st.device_final) == (_native.TIER_S, 128, 1, 1)
+
+
 def test_mixed_batch_against_oracle():
     prog = programs.program("ackermann")
     orules = O.rules_for("ackermann")
@@ -348,9 +372,9 @@ def test_errors_in_every_single_net_tier(ctas):
     # a cap that A(3,5)'s loop count exceeds, on a net large enough to use the tier
     prog = programs.program("ackermann")
     want = O.run_config(prog.build_input(3, 5), O.rules_for("ackermann"), collect=True)
-    cap = len(want.rows) // 2
-    with pytest.raises(errors.LoopCapExceeded):
-        evaluate(prog.build_input(3, 5), prog.rules, EngineConfig(max_loops=cap, ctas_per_net=ctas))
+    for cap in (len(want.rows) // 2, len(want.rows) - 1):  # the trailing no-op loop counts too
+        with pytest.raises(errors.LoopCapExceeded):
+            evaluate(prog.build_input(3, 5), prog.rules, EngineConfig(max_loops=cap, ctas_per_net=ctas))
     res = evaluate(prog.build_input(3, 5), prog.rules, EngineConfig(max_loops=len(want.rows), ctas_per_net=ctas))
     assert res.total_interactions == want.interactions
 
