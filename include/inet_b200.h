@@ -78,7 +78,9 @@ enum inet_status {
   INET_ERR_ARG = 5,          /* bad argument / malformed blob */
   INET_ERR_UNSUPPORTED = 6,  /* exceeds a device-engine limit */
   INET_ERR_NO_DEVICE = 7,    /* no CUDA device visible */
-  INET_ERR_STATE = 8         /* call order violated (e.g. fetch before reduce) */
+  INET_ERR_STATE = 8,        /* call order violated (e.g. fetch before reduce) */
+  INET_ERR_NAME = 9          /* NameDisciplineError       engine.py:169-183 (validate_phases); the
+                                variable's reference id in err_label_a (low) / err_label_b (high) */
 };
 
 typedef struct inet_ctx inet_ctx;
@@ -99,6 +101,11 @@ typedef struct inet_cfg {
                              communicates in the next round (engine.py:137-166), so rounds and
                              LoopStats rows are the reference's loops; 0: link to a fixpoint
                              within the round (fewer rounds) */
+  uint32_t reference_order; /* 1: tier R — the reference's equation list, in its order (var = var
+                               keys, merge orientation, first failing pair and residual order
+                               exactly as engine.py:106-166); 0: the fast tiers */
+  uint32_t validate_phases; /* 1: name discipline checked after both phases of every loop
+                               (engine.py:210-214); implies reference_order */
 } inet_cfg;
 
 /* Per-net outcome. */
@@ -114,7 +121,8 @@ typedef struct inet_net_stats {
   uint32_t n_residual;     /* parked equations at the fixpoint (input of finalize) */
   uint32_t cap_agents;     /* capacities the successful run used */
   uint32_t cap_vars;
-  uint32_t tier;           /* residency tier used: 0 S (shared), 1 M (mixed), 2 G (global), 3 C (cluster), 4 X (whole GPU) */
+  uint32_t tier;           /* residency tier used: 0 S (shared), 1 M (mixed), 2 G (global), 3 C (cluster), 4 X (whole GPU),
+                              5 R (reference order) */
   uint32_t jit;            /* 1 if the rule-set specialised kernel ran (else the interpreter) */
   uint32_t sm_mhz;         /* effective SM clock over this net's reduction (clock64 / globaltimer) */
   uint32_t device_final;   /* 1 if the normal form was finalized on the device (tier S), else the host did */

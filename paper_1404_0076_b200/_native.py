@@ -18,7 +18,7 @@ from .errors import DeviceError
 LIB_PATH = os.environ.get("INET_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                              "libinetb200.so")
 
-OK, NO_RULE, LOOP_CAP, ARENA, CUDA, ARG, UNSUPPORTED, NO_DEVICE, STATE = range(9)
+OK, NO_RULE, LOOP_CAP, ARENA, CUDA, ARG, UNSUPPORTED, NO_DEVICE, STATE, NAME = range(10)
 
 EXPORTS = (
     "inet_ctx_create",
@@ -57,6 +57,8 @@ class Cfg(C.Structure):
         ("max_retries", C.c_uint32),
         ("count_rules", C.c_uint32),
         ("exact_loops", C.c_uint32),
+        ("reference_order", C.c_uint32),
+        ("validate_phases", C.c_uint32),
     ]
 
 
@@ -158,7 +160,7 @@ def _ptr(a: np.ndarray, ctype=C.c_uint32):
 
 
 def _check(code: int, what: str) -> None:
-    if code not in (OK, NO_RULE, LOOP_CAP, ARENA):
+    if code not in (OK, NO_RULE, LOOP_CAP, ARENA, NAME):
         raise DeviceError(code, f"{what}: {strerror(code)}")
 
 
@@ -274,6 +276,13 @@ class Context:
         return _print_call(lambda b, cap, n: self.lib.inet_batch_print(self.h, net, names, arity, nl, b, cap, n),
                            "batch_print")
 
+    def result_counts(self, net: int) -> tuple[int, int, int]:
+        """(agents, interface terms, equations) of a finalized net's normal form, no copies."""
+        na, ni, ne = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(self.lib.inet_batch_result(self.h, net, None, C.byref(na), None, C.byref(ni), None, C.byref(ne)),
+               "batch_result")
+        return na.value, ni.value, ne.value
+
     def result(self, net: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         pa, pi, pe = _u32p(), _u32p(), _u32p()
         na, ni, ne = C.c_uint32(), C.c_uint32(), C.c_uint32()
@@ -354,7 +363,7 @@ def jit_compile(blob: np.ndarray, tier: int = 1, threads: int = 1024) -> tuple[i
     return code, log.value.decode(errors="replace")
 
 
-TIER_S, TIER_M, TIER_G, TIER_C, TIER_X = 0, 1, 2, 3, 4
+TIER_S, TIER_M, TIER_G, TIER_C, TIER_X, TIER_R = 0, 1, 2, 3, 4, 5
 
 
 def jit_precompile(blob: np.ndarray, tier: int, threads: int, exact_code: bool, count_rules: bool) -> tuple[int, str]:

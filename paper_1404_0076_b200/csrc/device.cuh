@@ -213,6 +213,9 @@ struct NetDesc {
   // device-side finalize (tier S): the net's interface; dev_final enables it
   const uint32_t* in_iface;
   uint32_t n_iface, dev_final;
+  // tier R (ordered.cuh): the per-net buffer of its list and stream arrays
+  uint8_t* rbuf;
+  uint32_t cap_list, cap_out;
 };
 
 // Launch-wide shape: ring sizes and the shared-memory capacities.
@@ -229,6 +232,8 @@ struct Shape {
   uint32_t promote_ints;          // tier M: give the net up to the cluster tier past this many interactions
   uint32_t detect_vh;             // stop with kNeedExact at the first var-headed merge (exact requested,
                                   // kernel without INET_EXACT_CODE)
+  uint32_t max_fresh;             // tier R: RuleSet.max_fresh (the reference's fresh-id block per equation)
+  uint32_t validate;              // tier R: name discipline after every phase (EngineConfig.validate_phases)
 };
 
 // Internal statuses (never returned to callers): a single-CTA run that outgrew

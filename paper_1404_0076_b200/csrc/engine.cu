@@ -16,6 +16,7 @@
 
 #include "../../include/inet_b200.h"
 #include "device.cuh"
+#include "ordered.cuh"
 #include "host.h"
 #include "jit.h"
 
@@ -60,6 +61,16 @@ __global__ void __launch_bounds__(kBlock) reduce_grid_kernel(const NetDesc* __re
   inetdev::reduce_grid_body<kBlock>(nets, n_nets, blob, sh, smem, sd);
 }
 
+// Tier R (ordered.cuh): the reference's list order, one CTA per net.
+template <int kBlock>
+__global__ void __launch_bounds__(kBlock) reduce_ordered_kernel(const NetDesc* __restrict__ nets, uint32_t n_nets,
+                                                                const uint32_t* __restrict__ blob, Shape sh) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ NetDesc sd;
+  __shared__ inetdev::RShared rs;
+  inetdev::reduce_ordered_body<kBlock>(nets, n_nets, blob, sh, smem, sd, rs);
+}
+
 using KernelFn = void (*)(const NetDesc*, uint32_t, const uint32_t*, Shape);
 
 KernelFn pick_cluster_kernel(uint32_t threads) {
@@ -94,6 +105,7 @@ KernelFn pick_kernel_t(uint32_t threads) {
 }
 
 KernelFn pick_kernel(uint32_t threads, int tier) {
+  if (tier == inetdev::kTierR) return threads <= 256 ? reduce_ordered_kernel<256> : reduce_ordered_kernel<1024>;
   if (tier == kTierC) return pick_cluster_kernel(threads);
   if (tier == inetdev::kTierX) return threads <= 256 ? reduce_grid_kernel<256> : reduce_grid_kernel<512>;
   if (tier == kTierS) return pick_kernel_t<kTierS>(threads);
@@ -177,8 +189,10 @@ struct inet_ctx {
   bool input_resident = false;
   // device state
   DevBuf d_in_agents, d_in_eqs, d_in_iface, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist,
-      d_defer, d_gs;
+      d_defer, d_gs, d_rbuf;
   bool grid_tier = false;  // the next layout is for tier X (global rings + grid state)
+  bool ordered_tier = false;  // the next layout is for tier R (list and stream arrays)
+  uint32_t cap_list = 0, cap_out = 0;  // tier R: equations per list / per output stream
   uint32_t cap_def = 0;  // deferred equations per net and round (reference loop mode)
   bool count_rules = false;
   std::vector<uint32_t> h_hist;
@@ -261,6 +275,8 @@ const char* inet_strerror(int status) {
       return "no CUDA device";
     case INET_ERR_STATE:
       return "call order violated";
+    case INET_ERR_NAME:
+      return "a variable occurs more than twice";
     default:
       return "unknown status";
   }
@@ -303,7 +319,7 @@ void inet_ctx_destroy(inet_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->d_blob, &c->d_in_agents, &c->d_in_eqs, &c->d_desc, &c->d_agents, &c->d_vslot, &c->d_aring,
-                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer, &c->d_gs})
+                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer, &c->d_gs, &c->d_rbuf})
     b->release();
   for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -426,6 +442,9 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
       (c->grid_tier && (c->d_aring.ensure(size_t(cap_agents) * 4) || c->d_vring.ensure(size_t(cap_vars) * 4) ||
                         c->d_gs.ensure(sizeof(inetdev::GridState) + 4096 * 4))))
     return INET_ERR_CUDA;
+  const size_t r_bytes =
+      c->ordered_tier ? inetdev::r_carve(nullptr, cap_agents, cap_vars, c->cap_list, c->cap_out, nullptr) : 0;
+  if (c->ordered_tier && c->d_rbuf.ensure(N * r_bytes)) return INET_ERR_CUDA;
   if (c->grid_tier) CUDA_TRY(cudaMemsetAsync(c->d_gs.p, 0, sizeof(inetdev::GridState) + 4096 * 4, c->stream));
   if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * hist_stride(c) * 4, c->stream));
   std::vector<NetDesc> desc(n);
@@ -458,6 +477,11 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.in_iface = static_cast<const uint32_t*>(c->d_in_iface.p) + c->iface_off[i];
     d.n_iface = static_cast<uint32_t>(c->iface_off[i + 1] - c->iface_off[i]);
     d.dev_final = c->dev_final ? 1u : 0u;
+    if (c->ordered_tier) {
+      d.rbuf = static_cast<uint8_t*>(c->d_rbuf.p) + size_t(i) * r_bytes;
+      d.cap_list = c->cap_list;
+      d.cap_out = c->cap_out;
+    }
     if (c->resume.on && n == 1) {
       // resume from tier M's hand-over: its arena, slot table and pending equations
       d.in_agents = d.agents;
@@ -537,13 +561,17 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
 }
 
 int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
-  const uint32_t threads = tier == kTierC ? cluster_threads(cfg) : tier == inetdev::kTierX ? 256u : auto_threads(c, cfg);
+  const uint32_t threads = tier == kTierC                ? cluster_threads(cfg)
+                           : tier == inetdev::kTierX     ? 256u
+                           : tier == inetdev::kTierR     ? (c->n_nets > 64 ? 256u : 1024u)
+                                                         : auto_threads(c, cfg);
   sh.threads = threads;
-  const void* jk = jit_kernel(c, tier, threads);
+  const void* jk = tier == inetdev::kTierR ? nullptr : jit_kernel(c, tier, threads);
   const void* fn = jk ? jk : reinterpret_cast<const void*>(pick_kernel(threads, tier));
   c->last_jit = jk != nullptr;
   c->last_threads = threads;
-  const size_t smem = size_t(plan_smem(sh, tier).words) * 4;
+  const size_t smem = tier == inetdev::kTierR ? (size_t(inetdev::align4(sh.rule_words)) + 16u * threads) * 4
+                                              : size_t(plan_smem(sh, tier).words) * 4;
   int dev_sms = 0, max_optin = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
@@ -696,7 +724,44 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   // Ackermann nets) never need it, and their rounds are the reference's loops.
   const bool exact = cfg && cfg->exact_loops;
   bool with_defer = exact && !c->jit_mode;  // the prebuilt kernels always carry the code
-  for (int pass = 0; pass < 2; ++pass) {
+  // Tier R: the reference's list order (ordered.cuh), capacities doubled on overflow.
+  const bool ordered = cfg && (cfg->reference_order || cfg->validate_phases);
+  if (ordered) {
+    const uint32_t pair_words = (c->n_labels * c->n_labels + 1) / 2;
+    uint32_t max_fresh = 0;
+    for (uint32_t r = 0; r < c->n_rules; ++r) max_fresh = std::max(max_fresh, (c->blob[4 + pair_words + r * 16] >> 16) & 0xFFu);
+    uint32_t ca = cfg->cap_agents ? cfg->cap_agents : (c->n_nets == 1 ? (1u << 16) : 4096u);
+    uint32_t cv = cfg->cap_vars ? cfg->cap_vars : (c->n_nets == 1 ? (1u << 16) : 4096u);
+    uint32_t cl = c->n_nets == 1 ? (1u << 14) : 2048u;
+    ca = std::max(ca, 2 * c->max_in_agents + 64);
+    cv = std::max(cv, 2 * c->max_in_vars + 64);
+    cl = std::max(cl, 2 * c->max_in_eqs + 64);
+    bool done = false;
+    for (uint32_t attempt = 0; !done; ++attempt) {
+      Shape sh = base_shape(c, max_loops);
+      sh.max_fresh = max_fresh;
+      sh.validate = cfg->validate_phases ? 1u : 0u;
+      c->ordered_tier = true;
+      c->cap_list = cl;
+      c->cap_out = 2 * cl;
+      c->cap_def = 0;
+      int st = layout(c, ca, cv, 1, cap_rounds);
+      if (st == INET_OK) st = launch(c, cfg, sh, inetdev::kTierR, &ms);
+      c->ordered_tier = false;
+      if (st) return st;
+      fetch_ctl();
+      c->tier = inetdev::kTierR;
+      c->shape = sh;
+      if (!any_oom()) done = true;
+      else if (attempt + 1 >= retries || uint64_t(ca) * 2 >= INET_VAR_BIT || uint64_t(cv) * 2 >= INET_VAR_BIT ||
+               uint64_t(cl) * 4 >= INET_VAR_BIT)
+        break;
+      ca *= 2;
+      cv *= 2;
+      cl *= 2;
+    }
+  }
+  for (int pass = 0; pass < 2 && !ordered; ++pass) {
   c->exact_code = with_defer || !c->jit_mode;
   bool done = false;
   c->promoted = false;
@@ -959,7 +1024,7 @@ int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
   try {
     if (!c || !c->reduced) return INET_ERR_STATE;
     // same tier, shape and capacities as the successful run: no growth expected
-    inet_cfg k = cfg ? *cfg : inet_cfg{1000000u, 0, 0, 0, 0, 0, 0, 0};
+    inet_cfg k = cfg ? *cfg : inet_cfg{1000000u, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     c->count_rules = k.count_rules != 0;
     CUDA_TRY(cudaSetDevice(c->device));
     const uint32_t cap_rounds = k.collect_stats ? rows_cap(c, k.max_loops) : 0u;
@@ -985,8 +1050,10 @@ int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
       c->cap_queue = cq;
     }
     c->grid_tier = c->tier == inetdev::kTierX;
+    c->ordered_tier = c->tier == inetdev::kTierR;
     int st = layout(c, c->cap_agents, c->cap_vars, c->cap_queue, cap_rounds);
     c->grid_tier = false;
+    c->ordered_tier = false;
     if (st) return st;
     Shape sh = c->shape;
     sh.max_rounds = k.max_loops;

@@ -29,6 +29,7 @@ from ._ref import core as _core
 from ._ref import engine as _ref_engine
 from ._ref import profile as _profile
 from .errors import (
+    UnsupportedNet,
     ArenaExhausted,
     DeviceError,
     LoopCapExceeded,
@@ -57,13 +58,21 @@ class EngineConfig(_ref_engine.EngineConfig):
     cluster size of a single net (0 = auto); ``exact_loops`` keeps the
     reference's loop structure (a merged equation that is still var-headed
     communicates in the next loop, so ``loops`` rows are the reference's),
-    False links to a fixpoint within a round.
+    False links to a fixpoint within a round. ``reference_order``: True runs
+    tier R, the reference's equation list in its own order (every count, row,
+    error and residual equation exactly as engine.py:106-166 produces them);
+    False the fast tiers only; None (default) picks tier R for rule sets and
+    nets where the order can show (``order_sensitive``) and reruns a net on
+    tier R after a fast run that failed with NoRuleForPair or left equations in
+    its normal form. ``validate_phases`` also runs on tier R (the name
+    discipline is checked on the device after both phases of every loop).
     """
 
     device: int = 0
     threads: int = 0
     ctas_per_net: int = 0
     exact_loops: bool = True
+    reference_order: Optional[bool] = None
 
 
 def as_engine_config(cfg) -> EngineConfig:
@@ -166,20 +175,177 @@ def prepare(configs: Sequence[Configuration], rules: RuleSet) -> Prepared:
     )
 
 
-def native_cfg(cfg: EngineConfig) -> _native.Cfg:
+def native_cfg(cfg: EngineConfig, ordered: bool = False) -> _native.Cfg:
     k = _native.Cfg()
     k.max_loops = max(0, min(int(cfg.max_loops), 0xFFFFFFFE))
     k.collect_stats = 1 if cfg.collect_stats else 0
     k.threads = getattr(cfg, "threads", 0)
     k.ctas_per_net = getattr(cfg, "ctas_per_net", 0)
     k.exact_loops = 1 if getattr(cfg, "exact_loops", True) else 0
+    k.reference_order = 1 if ordered else 0
+    k.validate_phases = 1 if cfg.validate_phases else 0
     return k
 
 
-def run_prepared(ctx: _native.Context, prep: Prepared, cfg: EngineConfig) -> tuple[int, float]:
+def run_prepared(ctx: _native.Context, prep: Prepared, cfg: EngineConfig, ordered: bool = False) -> tuple[int, float]:
     ctx.load_rules(prep.blob, key=prep.blob.tobytes())
     ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
-    return ctx.reduce(native_cfg(cfg))
+    return ctx.reduce(native_cfg(cfg, ordered))
+
+
+# ---------------------------------------------------------------------------
+# evaluation order: the fast tiers or tier R (the reference's list order)
+
+
+def _rule_equates_variables(rule) -> bool:
+    return any(is_var(e.lhs) and is_var(e.rhs) for e in rule.rhs)
+
+
+def order_sensitive(rules: RuleSet, configs: Sequence[Configuration] = ()) -> bool:
+    """Can the reference's own list order show in this run's results?
+
+    Yes when a var = var equation can arise — a rule right-hand side equating
+    two variables or an input equation between variables: the reference keys it
+    on the smaller variable id (engine.py:150-153), which decides the loop of
+    the merge, total_communications and the LoopStats rows — or when a
+    same-symbol rule is not symmetric in its two agents (it is applied in the
+    orientation of the equation, core.py:287-298, which for a merged pair is
+    the list order, engine.py:161-165). Such runs go to tier R.
+    """
+    from .flat import same_symbol_rule_is_symmetric
+
+    for rule in rules.rules.values():
+        if _rule_equates_variables(rule):
+            return True
+        if rule.lhs_a.name == rule.lhs_b.name and not same_symbol_rule_is_symmetric(rule):
+            return True
+    return any(is_var(e.lhs) and is_var(e.rhs) for c in configs for e in c.equations)
+
+
+def _wants_order(cfg, rules: RuleSet, configs: Sequence[Configuration]) -> Optional[bool]:
+    """True: tier R; False: the fast tiers only; None: fast tiers with exactness reruns."""
+    if cfg.validate_phases:
+        return True
+    forced = getattr(cfg, "reference_order", None)
+    if forced is not None:
+        return bool(forced)
+    if not getattr(cfg, "exact_loops", True):
+        # fixpoint linking is the device's own loop structure: only an
+        # orientation-dependent rule still needs the reference's order
+        from .flat import same_symbol_rule_is_symmetric
+
+        asym = any(r.lhs_a.name == r.lhs_b.name and not same_symbol_rule_is_symmetric(r) for r in rules.rules.values())
+        return True if asym else None
+    return True if order_sensitive(rules, configs) else None
+
+
+@dataclass
+class _NetOut:
+    stats: object
+    arrays: Optional[tuple] = None  # (agents, iface, eqs), host copies
+    text: Optional[str] = None
+    rows: Optional[np.ndarray] = None
+    n_eqs: int = 0
+
+
+def _reduce(ctx: _native.Context, prep: Prepared, cfg, ordered: bool, want_arrays: bool, want_text: bool,
+            finalize_threads: int = 0) -> tuple[list, float]:
+    """One launch over the prepared nets; per-net outcomes (results of the nets that succeeded)."""
+    _code, ms = run_prepared(ctx, prep, cfg, ordered)
+    n = len(prep.flats)
+    outs = [_NetOut(ctx.stats(i)) for i in range(n)]
+    ok = [o.stats.status == _native.OK for o in outs]
+    if want_arrays or want_text:
+        if all(ok):
+            ctx.finalize(0xFFFFFFFF, finalize_threads)
+        else:
+            for i in range(n):
+                if ok[i]:
+                    ctx.finalize(i, 1)
+        tab = label_table(prep.labels) if want_text else None
+        for i in range(n):
+            if not ok[i]:
+                continue
+            outs[i].n_eqs = ctx.result_counts(i)[2]
+            if want_arrays:
+                outs[i].arrays = ctx.result(i)
+            if want_text:
+                outs[i].text = ctx.text(i, tab)
+    if cfg.collect_stats:
+        for i in range(n):
+            if ok[i]:
+                outs[i].rows = ctx.rounds(i)
+    return outs, ms
+
+
+def _evaluate_nets(configs: Sequence[Configuration], rules: RuleSet, cfg, want_arrays: bool, want_text: bool,
+                   finalize_threads: int = 0):
+    """Reduce nets with the evaluation order ``cfg`` asks for; returns (prep, outs, device ms).
+
+    Fast tiers first when the order cannot matter (``_wants_order`` None), then
+    tier R for exactly the nets where the reference's list order could still
+    show: a NoRuleForPair (which pair of the loop fails first, and its
+    orientation, engine.py:88-92) and a normal form that keeps equations
+    (where finalize cuts a cycle depends on the list order, engine.py:313-355).
+    """
+    want = _wants_order(cfg, rules, configs)
+    if want is False:
+        from .flat import same_symbol_rule_is_symmetric
+
+        for rule in rules.rules.values():
+            if rule.lhs_a.name == rule.lhs_b.name and not same_symbol_rule_is_symmetric(rule):
+                raise UnsupportedNet(
+                    f"rule {rule.lhs_a.name}><{rule.lhs_b.name} is not symmetric in its two agents: with "
+                    "reference_order=False its result would depend on the orientation of a merged pair")
+    ctx = _native.context(getattr(cfg, "device", 0))
+    prep = prepare(configs, rules)
+    with ctx.lock:
+        outs, ms = _reduce(ctx, prep, cfg, bool(want), want_arrays, want_text, finalize_threads)
+        if want is None:
+            redo = [i for i, o in enumerate(outs)
+                    if o.stats.status == _native.NO_RULE or o.n_eqs > 0]
+            if redo:
+                sub = prepare([configs[i] for i in redo], rules)
+                souts, sms = _reduce(ctx, sub, cfg, True, want_arrays, want_text, finalize_threads)
+                for j, i in enumerate(redo):
+                    outs[i] = souts[j]
+                    outs[i].sub = (sub, j)
+                ms += sms
+    return prep, outs, ms
+
+
+def _final_of(prep: Prepared, out: _NetOut, i: int, config):
+    sub = getattr(out, "sub", None)
+    p, j = sub if sub is not None else (prep, i)
+    return unflatten(*out.arrays, p.labels, p.flats[j], term_classes(config))
+
+
+def _labels_of(prep: Prepared, out: _NetOut) -> Labels:
+    sub = getattr(out, "sub", None)
+    return sub[0].labels if sub is not None else prep.labels
+
+
+def _check_outcome(prep: Prepared, out: _NetOut, i: int, cfg, configs) -> None:
+    st = out.stats
+    if st.status == _native.OK:
+        return
+    if st.status == _native.NAME:
+        sub = getattr(out, "sub", None)
+        p, j = sub if sub is not None else (prep, i)
+        flat = p.flats[j]
+        refid = int(st.err_label_a) | (int(st.err_label_b) << 32)
+        n_in = len(flat.var_ids)
+        # tier R's reference ids: input variables keep their rank, fresh ones are
+        # numbered exactly as the reference's allocator numbers them (engine.py:196)
+        v = flat.var_ids[refid] if refid < n_in else flat.fresh_base + (refid - n_in)
+        raise NameDisciplineError(f"variable {v} occurs more than twice")
+    _raise_status(st.status, st, _labels_of(prep, out), cfg)
+
+
+def _loops(out: _NetOut) -> list:
+    if out.rows is None:
+        return []
+    return [LoopStats(j + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for j, r in enumerate(out.rows)]
 
 
 def evaluate(config: Configuration, rules: RuleSet, cfg: Optional[EngineConfig] = None) -> EvalResult:
@@ -189,25 +355,11 @@ def evaluate(config: Configuration, rules: RuleSet, cfg: Optional[EngineConfig] 
         raise SlotOverflow(
             f"slot_count {cfg.slot_count} is smaller than the largest rule rhs ({rules.max_rhs_size})"
         )
-    if cfg.validate_phases:
-        check_name_discipline(config.interface, config.equations)
-    ctx = _native.context(getattr(cfg, "device", 0))
-    prep = prepare([config], rules)
-    with ctx.lock:
-        code, _ms = run_prepared(ctx, prep, cfg)
-        st = ctx.stats(0)
-        if code != _native.OK:
-            _raise_status(code, st, prep.labels, cfg)
-        ctx.finalize(0, 1)
-        agents, iface, eqs = ctx.result(0)
-        rows = ctx.rounds(0) if cfg.collect_stats else None
-    final = unflatten(agents, iface, eqs, prep.labels, prep.flats[0], term_classes(config))
-    if cfg.validate_phases:
-        check_name_discipline(final.interface, final.equations)
-    loops = []
-    if rows is not None:
-        loops = [LoopStats(i + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for i, r in enumerate(rows)]
-    return EvalResult(final, loops, int(st.interactions), int(st.communications))
+    prep, outs, _ms = _evaluate_nets([config], rules, cfg, True, False, 1)
+    out = outs[0]
+    _check_outcome(prep, out, 0, cfg, [config])
+    final = _final_of(prep, out, 0, config)
+    return EvalResult(final, _loops(out), int(out.stats.interactions), int(out.stats.communications))
 
 
 @dataclass
@@ -265,40 +417,20 @@ def evaluate_batch(
         raise SlotOverflow(
             f"slot_count {cfg.slot_count} is smaller than the largest rule rhs ({rules.max_rhs_size})"
         )
-    ctx = _native.context(getattr(cfg, "device", 0))
-    prep = prepare(configs, rules)
-    with ctx.lock:
-        code, ms = run_prepared(ctx, prep, cfg)
-        if code != _native.OK:
-            for i in range(len(configs)):
-                st = ctx.stats(i)
-                if st.status != _native.OK:
-                    _raise_status(st.status, st, prep.labels, cfg)
-        ti, tc, mr, _nf = ctx.totals()
-        stats = [ctx.stats(i) for i in range(len(configs))]
-        finals = [None] * len(configs)
-        rows = [None] * len(configs)
-        texts = None
-        if as_terms or as_text:
-            ctx.finalize(0xFFFFFFFF, finalize_threads)
-        if as_terms:
-            for i in range(len(configs)):
-                finals[i] = ctx.result(i)
-        if as_text:
-            tab = label_table(prep.labels)
-            texts = [ctx.text(i, tab) for i in range(len(configs))]
-        if cfg.collect_stats:
-            rows = [ctx.rounds(i) for i in range(len(configs))]
-    out = []
-    for i, c in enumerate(configs):
-        final = None
-        if finals[i] is not None:
-            final = unflatten(*finals[i], prep.labels, prep.flats[i], term_classes(c))
-        loops = []
-        if rows[i] is not None:
-            loops = [LoopStats(j + 1, int(r[0]), int(r[1]), int(r[2]), int(r[3]) // 1000) for j, r in enumerate(rows[i])]
-        out.append(EvalResult(final, loops, int(stats[i].interactions), int(stats[i].communications)))
-    return BatchResult(out, ms, ti, tc, mr, texts)
+    prep, outs, ms = _evaluate_nets(configs, rules, cfg, as_terms, as_text, finalize_threads)
+    for i, o in enumerate(outs):
+        _check_outcome(prep, o, i, cfg, configs)
+    results = []
+    for i, (c, o) in enumerate(zip(configs, outs)):
+        final = _final_of(prep, o, i, c) if as_terms else None
+        results.append(EvalResult(final, _loops(o), int(o.stats.interactions), int(o.stats.communications)))
+    return BatchResult(
+        results, ms,
+        sum(r.total_interactions for r in results),
+        sum(r.total_communications for r in results),
+        max(int(o.stats.rounds) for o in outs),
+        [o.text for o in outs] if as_text else None,
+    )
 
 
 def evaluate_sharded(

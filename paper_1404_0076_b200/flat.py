@@ -115,9 +115,10 @@ def same_symbol_rule_is_symmetric(rule) -> bool:
     the order/orientation of its equations.
 
     The reference applies a same-symbol rule in the active equation's own
-    orientation (core.py:287-298). The device forms an active pair by a merge
-    in arrival order, so only rules whose result does not depend on the
-    orientation are accepted (``UnsupportedNet`` otherwise)."""
+    orientation (core.py:287-298). The fast tiers form an active pair by a
+    merge in arrival order, so nets with a rule whose result depends on the
+    orientation run on tier R, which keeps the reference's order
+    (engine.order_sensitive)."""
     swap = dict(zip(rule.a_vars, rule.b_vars))
     swap.update(zip(rule.b_vars, rule.a_vars))
     bound = list(rule.bound_vars)
@@ -143,11 +144,6 @@ def compile_rules(rules, labels: Labels) -> np.ndarray:
     rule_list = list(rules.rules.values())
     if len(rule_list) > MAX_RULES:
         raise UnsupportedNet(f"more than {MAX_RULES} rules")
-    for rule in rule_list:
-        if rule.lhs_a.name == rule.lhs_b.name and not same_symbol_rule_is_symmetric(rule):
-            raise UnsupportedNet(
-                f"rule {rule.lhs_a.name}><{rule.lhs_b.name} is not symmetric in its two agents: its result "
-                "would depend on the orientation of a pair formed by communication")
     pair = np.full(L * L + (L * L) % 2, 0xFFFF, dtype=np.uint16)
     recs = np.zeros((len(rule_list), 16), dtype=np.uint32)
     for ri, rule in enumerate(rule_list):

@@ -60,7 +60,8 @@ def test_random_rule_sets_compile(seed):
 def test_random_rule_sets_batch_against_oracle(seed):
     rules, nets = _case(seed)
     orules = O.compile_golden_rules(F.to_golden(rules))
-    out = evaluate_batch(nets, rules, EngineConfig(collect_stats=False), as_text=True)
+    # the fast tiers (these rule sets equate variables, so the default would pick tier R)
+    out = evaluate_batch(nets, rules, EngineConfig(collect_stats=False, reference_order=False), as_text=True)
     exact = 0
     for i, (net, res, text) in enumerate(zip(nets, out.results, out.texts)):
         want = O.run_config(net, orules, collect=False)
@@ -80,10 +81,34 @@ def test_random_rule_sets_single_net_tiers(seed, ctas):
     orules = O.compile_golden_rules(F.to_golden(rules))
     for net in nets:
         want = O.run_config(net, orules, collect=False)
-        res = evaluate(net, rules, EngineConfig(collect_stats=False, ctas_per_net=ctas))
+        res = evaluate(net, rules, EngineConfig(collect_stats=False, ctas_per_net=ctas, reference_order=False))
         text = print_configuration(res.final)
         assert res.total_interactions == want.interactions
         assert _same_normal_form(text, res.final, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", SEEDS)
+def test_random_rule_sets_reference_order_byte_identical(seed):
+    """Tier R (the default for these rule sets, which equate variables): every
+    count and every printed normal form — cyclic ones included — byte-identical
+    to the oracle, which follows the reference's list order (no isomorphism
+    fallback)."""
+    rules, nets = _case(seed)
+    orules = O.compile_golden_rules(F.to_golden(rules))
+    out = evaluate_batch(nets, rules, EngineConfig(collect_stats=True), as_text=True)
+    cyclic = 0
+    for i, (net, res, text) in enumerate(zip(nets, out.results, out.texts)):
+        want = O.run_config(net, orules, collect=True)
+        assert res.total_interactions == want.interactions, (seed, i)
+        assert res.total_communications == want.communications, (seed, i)
+        assert [(s.interactions, s.communications, s.live_equations) for s in res.loops] == \
+            [tuple(r) for r in want.rows], (seed, i)
+        assert text == want.printed(), (seed, i)
+        cyclic += " = " in text
+    ctx = _native.context(0)
+    assert ctx.stats(0).tier == _native.TIER_R
+    del cyclic
 
 
 def test_netgraph_canonical_form():

@@ -82,10 +82,11 @@ def test_ackermann_communications_equal_reference():
             assert evaluate(config, rules).total_communications == case["communications"], case["name"]
 
 
-def test_arith_551_nets_one_launch():
+@pytest.mark.parametrize("order", [None, False])
+def test_arith_551_nets_one_launch(order):
     rules = to_rules(PROGRAMS["arith"])
     configs = [to_config(c["net"]) for c in ARITH]
-    out = evaluate_batch(configs, rules, EngineConfig(collect_stats=False))
+    out = evaluate_batch(configs, rules, EngineConfig(collect_stats=False, reference_order=order))
     for case, res in zip(ARITH, out.results):
         assert res.total_interactions == case["interactions"], case["name"]
         assert _sha(print_configuration(res.final)) == case["print_sha256"], case["name"]
@@ -250,6 +251,7 @@ def test_cluster_tier_fixtures(g):
         config, rules = _case_inputs(case)
         kw = dict(case.get("engine_config", {}))
         kw["ctas_per_net"] = g
+        kw["reference_order"] = False  # this tier, not tier R
         cfg = EngineConfig(**kw)
         if "error" in case:
             with pytest.raises(getattr(errors, case["error"])) as ei:
@@ -283,7 +285,7 @@ def test_cluster_tier_random_arith_against_oracle():
     rng = random.Random(99)
     for _ in range(40):
         net = _random_arith_net(rng, rules.symbols, rng.choice([8, 40, 200, 1000]))
-        res = evaluate(net, rules, EngineConfig(ctas_per_net=8, collect_stats=False))
+        res = evaluate(net, rules, EngineConfig(ctas_per_net=8, collect_stats=False, reference_order=False))
         want = O.run_config(net, orules, collect=False)
         assert res.total_interactions == want.interactions
         assert print_configuration(res.final) == want.printed()
@@ -334,6 +336,7 @@ def test_whole_gpu_tier_fixtures():
         config, rules = _case_inputs(case)
         kw = dict(case.get("engine_config", {}))
         kw["ctas_per_net"] = 148
+        kw["reference_order"] = False  # this tier, not tier R
         cfg = EngineConfig(**kw)
         if "error" in case:
             with pytest.raises(getattr(errors, case["error"])):
@@ -363,11 +366,11 @@ def test_errors_in_every_single_net_tier(ctas):
     """LoopCapExceeded / NoRuleForPair from tiers M, C and X as the reference's classes."""
     loop = parse_program("Loop >< Z => Loop = Z;\nnet : Loop = Z;")
     with pytest.raises(errors.LoopCapExceeded) as ei:
-        evaluate(loop.net, loop.rules, EngineConfig(max_loops=7, ctas_per_net=ctas))
+        evaluate(loop.net, loop.rules, EngineConfig(max_loops=7, ctas_per_net=ctas, reference_order=False))
     assert ei.value.max_loops == 7
     bad = parse_program("A >< B => ;\nnet : A = C;")
     with pytest.raises(errors.NoRuleForPair) as ei:
-        evaluate(bad.net, bad.rules, EngineConfig(ctas_per_net=ctas))
+        evaluate(bad.net, bad.rules, EngineConfig(ctas_per_net=ctas, reference_order=False))
     assert ei.value.pair == ("A", "C")
     # a cap that A(3,5)'s loop count exceeds, on a net large enough to use the tier
     prog = programs.program("ackermann")
