@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import concurrent.futures as cf
+import hashlib
 import json
 import os
 import statistics
@@ -295,6 +296,26 @@ def workload_spec(name: str):
                           "l2": "flushed between steps (256 MiB write)"}
 
 
+def nat_text(height: int) -> str:
+    """print_configuration of the normal form S^height(Z) (lang.py:371-396)."""
+    return "net " + "S(" * height + "Z" + ")" * height + " : ;"
+
+
+def timed_outcomes(ctx, prep, n_nets: int, height: int) -> list:
+    """(interactions, text sha prefix) of every net of the last launch, each text checked."""
+    from paper_1404_0076_b200 import engine
+
+    ctx.finalize(0xFFFFFFFF, 0)
+    tab = engine.label_table(prep.labels)
+    want = nat_text(height)
+    out = []
+    for i in range(n_nets):
+        text = ctx.text(i, tab)
+        assert text == want, (i, text[:80])
+        out.append((int(ctx.stats(i).interactions), hashlib.sha256(text.encode()).hexdigest()[:16]))
+    return out
+
+
 def check_normal_forms(ctx, n_nets: int, height: int, sample: int = 64) -> None:
     """Every sampled net must reduce to S^height(Z) with no residual equation."""
     ctx.finalize(0xFFFFFFFF, 0)
@@ -366,6 +387,12 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # the timed launches' own outcome (the count_rules=0 kernel variant): status and
+    # totals of the last timed launch, and every net's printed normal form
+    ctx.collect()
+    ti_t, tc_t, _mr_t, nfail_t = ctx.totals()
+    assert nfail_t == 0 and ti_t == ti and tc_t == tc, (ti_t, tc_t, nfail_t)
+    outcomes = timed_outcomes(ctx, prep, n_nets, height)
     my_ms = sum(times)
     max_ms = shard.max_over_ranks(my_ms, device=f"cuda:{dev}")
     # interactions of one step, all ranks (each rank verified its own count above)
@@ -385,8 +412,28 @@ def run_ours(args) -> None:
         e2e_times.append(time.perf_counter() - t0)
         assert code == _native.OK and len(agents0) == height + 1
         h2d, d2h = ctx.io_bytes()
+        assert ctx.totals()[0] == ti
     e2e_max = shard.max_over_ranks(sum(e2e_times), device=f"cuda:{dev}")
     e2e_value = total_interactions * len(e2e_times) / e2e_max
+
+    # e2e through the Python API a user calls: evaluate_batch(as_text=True) on
+    # this rank's shard — flattening the reference's term objects, H2D, the
+    # reduction, D2H, finalize and the canonical text of every net
+    api_times = []
+    for _ in range(max(1, args.api_steps)):
+        t0 = time.perf_counter()
+        out = engine.evaluate_batch(configs, prog.rules, ecfg, as_terms=False, as_text=True)
+        api_times.append(time.perf_counter() - t0)
+        assert out.total_interactions == ti
+    api_max = shard.max_over_ranks(min(api_times), device=f"cuda:{dev}")
+    api_value = total_interactions / api_max
+
+    # final result gather: per-net (interactions, text sha) to rank 0
+    gathered = shard.gather_outcomes(outcomes, world)
+    if rank == 0:
+        want_sha = hashlib.sha256(nat_text(height).encode()).hexdigest()[:16]
+        assert len(gathered) == (BATCH_NETS if args.workload == "batch" else 1)
+        assert all(o == (per_net, want_sha) for o in gathered), "gathered outcomes differ"
 
     peak, peak_kind = load_peaks()
     achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9
@@ -414,6 +461,13 @@ def run_ours(args) -> None:
             "e2e": {"value": e2e_value, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "path": "C ABI inet_batch_load+inet_batch_reduce+inet_batch_finalize, host flat buffers"},
+            "e2e_api": {"value": api_value, "unit": "interactions/s", "ms": 1000 * api_max,
+                        "path": "paper_1404_0076_b200.evaluate_batch(configs, rules, as_terms=False, as_text=True): "
+                                "flatten + H2D + reduce + D2H + finalize + canonical text, best of "
+                                f"{len(api_times)}"},
+            "gather": {"nets": len(gathered), "bytes_per_net": 24,
+                       "what": "per-net (interactions, sha256 prefix of the printed normal form) gathered to "
+                               "rank 0 after the timed region; every net checked against S^509(Z)"},
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
@@ -444,11 +498,30 @@ def run_ours(args) -> None:
                 flush_l2()
                 best.append(c2.rerun(kk))
             ms = min(best)
-            singles[label] = {"interactions": golden, "rounds": st.rounds, "device_ms": ms, "tier": "SMGCX"[st.tier],
+            singles[label] = {"interactions": golden, "rounds": st.rounds, "device_ms": ms, "tier": "SMGCXR"[st.tier],
                               "sm_mhz": st.sm_mhz,
                               "agent_hw": st.agent_hw, "var_hw": st.var_hw,
                               "interactions_per_s": golden / (ms / 1000.0),
                               "us_per_round": 1000.0 * ms / max(st.rounds, 1)}
+            if engine.order_sensitive(p.rules, [p.build_input(*pparams)]):
+                # what evaluate() runs by default for this net: tier R, the reference's order
+                kr = engine.native_cfg(EngineConfig(collect_stats=False), ordered=True)
+                code, _ = c2.reduce(kr)
+                st_r = c2.stats(0)
+                assert code == _native.OK and st_r.interactions == golden
+                ms_r = min(c2.rerun(kr) for _ in range(3))
+                singles[label]["reference_order"] = {
+                    "device_ms": ms_r, "rounds": st_r.rounds, "communications": int(st_r.communications),
+                    "interactions_per_s": golden / (ms_r / 1000.0), "us_per_loop": 1000.0 * ms_r / max(st_r.rounds, 1)}
+            # end to end through the public API (default evaluation order), host objects in, text out
+            e2e = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                _text, ints, _comms = engine.evaluate_text(p.build_input(*pparams), p.rules)
+                e2e.append(time.perf_counter() - t0)
+                assert ints == golden
+            singles[label]["e2e_ms"] = 1000.0 * min(e2e)
+            singles[label]["e2e_path"] = "evaluate_text(config, rules): flatten + H2D + reduce + D2H + finalize + print"
             c2.close()
         line["single_nets"] = singles
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -475,6 +548,7 @@ def main():
     ap.add_argument("--workload", choices=["batch", "a310", "a38", "fib18"], default="batch")
     ap.add_argument("--threads", type=int, default=0, help="CTA size per net (0 = auto)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--api-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

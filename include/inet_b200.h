@@ -195,6 +195,9 @@ int inet_batch_rerun(inet_ctx* ctx, const inet_cfg* cfg, float* device_ms);
 
 /* EvalResult.total_interactions / total_communications and the error of net i
  * (engine.py:51-56; errors.py:46-56). */
+/* Fetch the outcome of the last launch (after inet_batch_rerun, which only
+ * times it): per-net statistics and results, as inet_batch_reduce leaves them. */
+int inet_batch_collect(inet_ctx* ctx);
 int inet_batch_stats(inet_ctx* ctx, uint32_t net, inet_net_stats* out);
 /* Interactions per rule of net i (needs cfg.count_rules); counts[n_rules]. */
 int inet_batch_rule_counts(inet_ctx* ctx, uint32_t net, uint64_t* counts, uint32_t n_rules);

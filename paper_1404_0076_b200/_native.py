@@ -33,6 +33,7 @@ EXPORTS = (
     "inet_batch_load",
     "inet_batch_reduce",
     "inet_batch_rerun",
+    "inet_batch_collect",
     "inet_batch_stats",
     "inet_batch_rule_counts",
     "inet_batch_io_bytes",
@@ -113,6 +114,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             "inet_batch_load": (C.c_int, [C.c_void_p, C.c_uint32, _u32p, _u64p, _u32p, _u64p, _u32p, _u64p, _u32p]),
             "inet_batch_reduce": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
             "inet_batch_rerun": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
+            "inet_batch_collect": (C.c_int, [C.c_void_p]),
             "inet_batch_stats": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(NetStats)]),
             "inet_batch_totals": (C.c_int, [C.c_void_p, _u64p, _u64p, _u32p, _u32p]),
             "inet_batch_rule_counts": (C.c_int, [C.c_void_p, C.c_uint32, _u64p, C.c_uint32]),
@@ -236,6 +238,12 @@ class Context:
         ms = C.c_float()
         _check(self.lib.inet_batch_rerun(self.h, C.byref(cfg), C.byref(ms)), "batch_rerun")
         return ms.value
+
+    def collect(self) -> int:
+        """Statistics and results of the last launch (e.g. the last timed rerun)."""
+        code = self.lib.inet_batch_collect(self.h)
+        _check(code, "batch_collect")
+        return code
 
     def stats(self, net: int) -> NetStats:
         s = NetStats()

@@ -674,6 +674,7 @@ uint32_t rows_cap(const inet_ctx* c, uint32_t max_loops) {
 }
 
 int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch);
+int finish_run(inet_ctx* c, bool fetch);
 
 int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   if (!c) return INET_ERR_STATE;
@@ -927,6 +928,12 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   }
   if (c->promoted && c->tier != kTierC) c->promoted = false;  // the cluster fell through: no prefix
   if (device_ms) *device_ms = ms + (c->promoted ? c->promo_ms : 0.0f);
+  return finish_run(c, fetch);
+}
+
+// Per-net statistics from the fetched control blocks and, with fetch, the
+// result arrays (arena prefixes, residual equations, rows) of the last launch.
+int finish_run(inet_ctx* c, bool fetch) {
   c->stats.assign(c->n_nets, inet_net_stats{});
   c->dev_rows.assign(c->n_nets, 0);
   int first = INET_OK;
@@ -1062,6 +1069,21 @@ int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
     if (st) return st;
     if (device_ms) *device_ms = ms + pre_ms;
     return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
+}
+
+int inet_batch_collect(inet_ctx* c) {
+  try {
+    if (!c || !c->reduced) return INET_ERR_STATE;
+    CUDA_TRY(cudaSetDevice(c->device));
+    c->ctl.assign(c->n_nets, NetCtl{});
+    CUDA_TRY(cudaMemcpy(c->ctl.data(), c->d_ctl.p, c->n_nets * sizeof(NetCtl), cudaMemcpyDeviceToHost));
+    c->collect_stats = c->cap_rounds != 0;
+    return finish_run(c, true);
   } catch (const std::bad_alloc&) {
     return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
   } catch (...) {
