@@ -728,6 +728,8 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   // Tier R: the reference's list order (ordered.cuh), capacities doubled on overflow.
   const bool ordered = cfg && (cfg->reference_order || cfg->validate_phases);
   if (ordered) {
+    c->resume.on = false;  // a hand-over of an earlier single-net run must not leak into this layout
+    c->promoted = false;
     const uint32_t pair_words = (c->n_labels * c->n_labels + 1) / 2;
     uint32_t max_fresh = 0;
     for (uint32_t r = 0; r < c->n_rules; ++r) max_fresh = std::max(max_fresh, (c->blob[4 + pair_words + r * 16] >> 16) & 0xFFu);

@@ -19,9 +19,11 @@
 //                in list order, to three streams — agent=agent (P, the next
 //                list's head), parked singles whose key is unchanged (A, still
 //                sorted from the previous loop) and everything else (B);
-//   communication  B is normalised (var left, smaller refid left), stably
-//                radix-sorted by key refid; A and B are merged by (key, list
-//                position) with binary searches; runs of equal keys fold as
+//   communication  B is normalised (var left, smaller refid left) and stably
+//                sorted by key refid (rank counting in shared memory for a
+//                small stream, an LSD radix sort otherwise); A and B are
+//                merged by (key, list position) along a merge path (each
+//                thread walks its chunk of A); runs of equal keys fold as
 //                reduce_by_key does (a run x=t, x=u -> t = u; longer runs keep
 //                the last two right-hand sides, like the reference's fold);
 //   next list    P ++ folded runs.
@@ -150,6 +152,8 @@ __device__ __forceinline__ void chunk_of(uint32_t n, uint32_t& lo, uint32_t& hi)
 
 __device__ __forceinline__ bool r_is_var(uint32_t t) { return (t & kVar) != 0; }
 
+constexpr uint32_t kSmallB = 256;  // stream B sorted in shared memory up to this size
+
 // Shared state of the running loop (one copy per CTA).
 struct RShared {
   uint32_t scan[8 * 33 + 8];
@@ -157,6 +161,10 @@ struct RShared {
   uint32_t err_i;                // first failing active entry (NoRuleForPair)
   unsigned long long bad_var;    // smallest refid occurring more than twice (validate)
   uint32_t flag;
+  // a small stream B, sorted in shared memory
+  unsigned long long sb_key[kSmallB];
+  uint32_t sb_pos[kSmallB];
+  uint2 sb_eq[kSmallB];
 };
 
 // Source k of a rule template -> term ref (include/inet_b200.h source coding).
@@ -197,6 +205,36 @@ __device__ __forceinline__ unsigned long long r_normalise(const RArrays& R, uint
   }
   if (!lv) e = make_uint2(e.y, e.x);
   return R.refid[e.x & ~kVar];
+}
+
+// Sort a small stream B (n <= kSmallB) into shared memory: each item's rank is
+// the number of items with a smaller key, or an equal key earlier in the
+// stream (B is written in list order, so this is the stable order).
+__device__ void r_sort_small(const RArrays& R, uint32_t n, RShared& S) {
+  unsigned long long k = 0;
+  uint32_t p = 0;
+  uint2 e = make_uint2(0, 0);
+  const uint32_t b = threadIdx.x;
+  if (b < n) {
+    k = R.bkey[0][b];
+    p = R.bpos[0][b];
+    e = R.beq[0][b];
+    S.sb_key[b] = k;
+  }
+  __syncthreads();
+  uint32_t rank = 0;
+  if (b < n)
+    for (uint32_t j = 0; j < n; ++j) {
+      const unsigned long long kj = S.sb_key[j];
+      rank += kj < k || (kj == k && j < b);
+    }
+  __syncthreads();
+  if (b < n) {
+    S.sb_key[rank] = k;
+    S.sb_pos[rank] = p;
+    S.sb_eq[rank] = e;
+  }
+  __syncthreads();
 }
 
 // Stable LSD radix sort of stream B by key (4-bit digits over the key range).
@@ -502,19 +540,51 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       }
     }
     // ---- communication: sort B by key (stable), merge with A, fold runs
-    const int sb = r_sort_b(R, nB, S, hist);
-    const unsigned long long* bk = R.bkey[sb];
-    const uint32_t* bp = R.bpos[sb];
-    const uint2* be = R.beq[sb];
-    for (uint32_t a = threadIdx.x; a < nA; a += T) {
-      const uint32_t p = a + r_rank(bk, bp, nB, R.akey[a], R.apos[a]);
-      R.skey[p] = R.akey[a];
-      R.seq[p] = R.aeq[a];
+    const unsigned long long* bk;
+    const uint32_t* bp;
+    const uint2* be;
+    if (nB <= kSmallB && T >= kSmallB) {
+      r_sort_small(R, nB, S);
+      bk = S.sb_key;
+      bp = S.sb_pos;
+      be = S.sb_eq;
+    } else {
+      const int sb = r_sort_b(R, nB, S, hist);
+      bk = R.bkey[sb];
+      bp = R.bpos[sb];
+      be = R.beq[sb];
     }
-    for (uint32_t b = threadIdx.x; b < nB; b += T) {
-      const uint32_t p = b + r_rank(R.akey, R.apos, nA, bk[b], bp[b]);
-      R.skey[p] = bk[b];
-      R.seq[p] = be[b];
+    // merge path: thread t merges its chunk of A with the B items that sort
+    // before the chunk's end (A is sorted from the last loop, keys unique)
+    chunk_of(nA, lo, hi);
+    if (nA == 0) {
+      for (uint32_t b = threadIdx.x; b < nB; b += T) {
+        R.skey[b] = bk[b];
+        R.seq[b] = be[b];
+      }
+    } else if (lo < hi) {
+      const uint32_t jb = lo == 0 ? 0u : r_rank(bk, bp, nB, R.akey[lo], R.apos[lo]);
+      const uint32_t je = hi == nA ? nB : r_rank(bk, bp, nB, R.akey[hi], R.apos[hi]);
+      uint32_t i = lo, j = jb;
+      unsigned long long ka = R.akey[i];
+      uint32_t pa = R.apos[i];
+      while (i < hi || j < je) {
+        bool take_b = j < je;
+        if (take_b && i < hi) take_b = bk[j] < ka || (bk[j] == ka && bp[j] < pa);
+        if (take_b) {
+          R.skey[i + j] = bk[j];
+          R.seq[i + j] = be[j];
+          ++j;
+        } else {
+          R.skey[i + j] = ka;
+          R.seq[i + j] = R.aeq[i];
+          ++i;
+          if (i < hi) {
+            ka = R.akey[i];
+            pa = R.apos[i];
+          }
+        }
+      }
     }
     __syncthreads();
     const uint32_t nS = nA + nB;

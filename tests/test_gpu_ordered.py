@@ -32,7 +32,6 @@ from paper_1404_0076_b200 import (
 )
 from paper_1404_0076_b200 import errors
 from paper_1404_0076_b200._ref import bench as programs
-from paper_1404_0076_b200._ref import core as ref_core
 
 pytestmark = pytest.mark.gpu
 
@@ -182,4 +181,3 @@ def test_tier_r_batch_reproducible_ids():
     two = evaluate_batch(nets, prog.rules, EngineConfig(reference_order=True), as_text=True)
     assert one.texts == two.texts
     assert [r.total_communications for r in one.results] == [r.total_communications for r in two.results]
-    del ref_core
