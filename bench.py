@@ -218,6 +218,22 @@ def ncu_traffic(workload: str):
         return None
 
 
+def ncu_issue(workload: str):
+    """Instruction-issue figures of the workload's timed kernel(s) from the committed
+    ncu capture (profiles/issue.json, tools/ncu_issue.py): what binds these kernels
+    is issue and latency, not HBM."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as fh:
+            rec = json.load(fh).get(workload)
+    except (OSError, ValueError):
+        return None
+    if rec is None:
+        return None
+    keep = ("issue_active_pct_of_active_smsp", "lanes_active_avg", "thread_inst_per_interaction", "warp_inst",
+            "duration_ns", "kernels", "source")
+    return {k: rec[k] for k in keep if k in rec}
+
+
 def cpu_sample(program_name: str, params, seconds: float, threads: int) -> dict:
     """Time the oracle (reference algorithm, C++ port) on the host for ~seconds."""
     from oracle import oracle as O
@@ -473,6 +489,7 @@ def run_ours(args) -> None:
                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": alg_bytes,
+                         "issue": ncu_issue(args.workload),
                          "note": "SURVEY.md §8(d) bytes: per-rule (read+write) x device rule histogram "
                                  "+ 24 B per communication"},
             "clocks": clocks.summary(),
@@ -521,6 +538,8 @@ def run_ours(args) -> None:
                 e2e.append(time.perf_counter() - t0)
                 assert ints == golden
             singles[label]["e2e_ms"] = 1000.0 * min(e2e)
+            if label == "A(3,10)":
+                singles[label]["issue"] = ncu_issue("a310")
             singles[label]["e2e_path"] = "evaluate_text(config, rules): flatten + H2D + reduce + D2H + finalize + print"
             c2.close()
         line["single_nets"] = singles

@@ -105,7 +105,8 @@ KernelFn pick_kernel_t(uint32_t threads) {
 }
 
 KernelFn pick_kernel(uint32_t threads, int tier) {
-  if (tier == inetdev::kTierR) return threads <= 256 ? reduce_ordered_kernel<256> : reduce_ordered_kernel<1024>;
+  if (tier == inetdev::kTierR)
+    return threads <= 256 ? reduce_ordered_kernel<256> : threads <= 512 ? reduce_ordered_kernel<512> : reduce_ordered_kernel<1024>;
   if (tier == kTierC) return pick_cluster_kernel(threads);
   if (tier == inetdev::kTierX) return threads <= 256 ? reduce_grid_kernel<256> : reduce_grid_kernel<512>;
   if (tier == kTierS) return pick_kernel_t<kTierS>(threads);
@@ -517,6 +518,13 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
   return c->n_nets >= 16 ? 512 : 256;
 }
 
+// CTA size of tier R for a few nets (env INET_B200_RTHREADS overrides; measured).
+uint32_t tier_r_threads(const inet_cfg* cfg) {
+  if (cfg && cfg->threads) return cfg->threads <= 256 ? 256u : cfg->threads <= 512 ? 512u : 1024u;
+  if (const char* e = std::getenv("INET_B200_RTHREADS")) return static_cast<uint32_t>(std::atoi(e));
+  return 512u;
+}
+
 // CTA size of tier C (one CTA per SM of the cluster).
 uint32_t cluster_threads(const inet_cfg* cfg) {
   const uint32_t t = cfg && cfg->threads ? cfg->threads : 256;
@@ -563,7 +571,7 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
 int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
   const uint32_t threads = tier == kTierC                ? cluster_threads(cfg)
                            : tier == inetdev::kTierX     ? 256u
-                           : tier == inetdev::kTierR     ? (c->n_nets > 64 ? 256u : 1024u)
+                           : tier == inetdev::kTierR     ? (c->n_nets > 64 ? 256u : tier_r_threads(cfg))
                                                          : auto_threads(c, cfg);
   sh.threads = threads;
   const void* jk = tier == inetdev::kTierR ? nullptr : jit_kernel(c, tier, threads);

@@ -153,6 +153,8 @@ __device__ __forceinline__ void chunk_of(uint32_t n, uint32_t& lo, uint32_t& hi)
 __device__ __forceinline__ bool r_is_var(uint32_t t) { return (t & kVar) != 0; }
 
 constexpr uint32_t kSmallB = 256;  // stream B sorted in shared memory up to this size
+constexpr uint32_t kRB = 4;        // list entries whose loads are batched (interaction passes)
+constexpr uint32_t kRW = 8;        // sorted keys a thread prefetches for the fold
 
 // Shared state of the running loop (one copy per CTA).
 struct RShared {
@@ -395,37 +397,61 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
     chunk_of(nE, lo, hi);
     // 0 P outputs, 1 A outputs, 2 B outputs, 3 agents taken, 4 agents freed, 5 variables taken, 6 active
     uint32_t cnt[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t i = lo; i < hi; ++i) {
-      const uint2 e = E[i];
-      if (r_is_var(e.x) || r_is_var(e.y)) {
-        cnt[F[i] ? 1 : 2] += 1;
-        continue;
+    // entries are processed in batches of kRB whose loads are all issued before
+    // any is used: one L2 round trip per batch instead of one per entry
+    for (uint32_t i0 = lo; i0 < hi; i0 += kRB) {
+      uint2 ev[kRB];
+      uint8_t fv[kRB];
+      uint4 av[kRB], bv[kRB];
+#pragma unroll
+      for (uint32_t k = 0; k < kRB; ++k) {
+        ev[k] = i0 + k < hi ? E[i0 + k] : make_uint2(kVar, kVar);
+        fv[k] = i0 + k < hi ? F[i0 + k] : 0;
       }
-      RRewrite w;
-      w.A = d.agents[e.x];
-      w.B = d.agents[e.y];
-      const uint32_t t = pair[w.A.x * sh.n_labels + w.B.x];
-      if (t == 0xFFFFu) {
-        atomicMin(&S.err_i, i);
-        break;  // later entries of this chunk cannot be the first failure
+#pragma unroll
+      for (uint32_t k = 0; k < kRB; ++k) {
+        const bool act = !r_is_var(ev[k].x) && !r_is_var(ev[k].y);
+        av[k] = act ? d.agents[ev[k].x] : make_uint4(0, 0, 0, 0);
+        bv[k] = act ? d.agents[ev[k].y] : make_uint4(0, 0, 0, 0);
       }
-      if (t & 1u) {
-        const uint4 tmp = w.A;
-        w.A = w.B;
-        w.B = tmp;
+      bool failed = false;
+#pragma unroll
+      for (uint32_t k = 0; k < kRB; ++k) {
+        const uint32_t i = i0 + k;
+        if (i >= hi || failed) continue;
+        const uint2 e = ev[k];
+        if (r_is_var(e.x) || r_is_var(e.y)) {
+          cnt[fv[k] ? 1 : 2] += 1;
+          continue;
+        }
+        RRewrite w;
+        w.A = av[k];
+        w.B = bv[k];
+        const uint32_t t = pair[w.A.x * sh.n_labels + w.B.x];
+        if (t == 0xFFFFu) {
+          atomicMin(&S.err_i, i);
+          failed = true;  // later entries of this chunk cannot be the first failure
+          continue;
+        }
+        if (t & 1u) {
+          const uint4 tmp = w.A;
+          w.A = w.B;
+          w.B = tmp;
+        }
+        const uint32_t* Rr = rules + (t >> 1) * kRuleWords;
+        const uint32_t hdr = Rr[0];
+        const uint32_t nn = hdr & 0xFFu, ne = (hdr >> 8) & 0xFFu, nf = (hdr >> 16) & 0xFFu;
+        for (uint32_t q = 0; q < ne; ++q) {
+          const uint32_t h = (Rr[9 + (q >> 1)] >> ((q & 1) * 16)) & 0xFFFFu;
+          const bool act = w.src_is_agent(h & 0xFFu) && w.src_is_agent(h >> 8);
+          cnt[act ? 0 : 2] += 1;
+        }
+        cnt[3] += nn > 2 ? nn - 2 : 0;
+        cnt[4] += nn < 2 ? 2 - nn : 0;
+        cnt[5] += nf;
+        cnt[6] += 1;
       }
-      const uint32_t* Rr = rules + (t >> 1) * kRuleWords;
-      const uint32_t hdr = Rr[0];
-      const uint32_t nn = hdr & 0xFFu, ne = (hdr >> 8) & 0xFFu, nf = (hdr >> 16) & 0xFFu;
-      for (uint32_t q = 0; q < ne; ++q) {
-        const uint32_t h = (Rr[9 + (q >> 1)] >> ((q & 1) * 16)) & 0xFFFFu;
-        const bool act = w.src_is_agent(h & 0xFFu) && w.src_is_agent(h >> 8);
-        cnt[act ? 0 : 2] += 1;
-      }
-      cnt[3] += nn > 2 ? nn - 2 : 0;
-      cnt[4] += nn < 2 ? 2 - nn : 0;
-      cnt[5] += nf;
-      cnt[6] += 1;
+      if (failed) break;
     }
     uint32_t off[7], tot[7];
 #pragma unroll
@@ -446,79 +472,101 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       break;
     }
     // ---- interaction, pass 2: rewrite in list order, emit the three streams
-    for (uint32_t i = lo; i < hi; ++i) {
-      uint2 e = E[i];
-      const uint32_t opos = i * kRPos;
-      if (r_is_var(e.x) || r_is_var(e.y)) {
-        if (F[i]) {
-          R.aeq[off[1]] = e;
-          R.akey[off[1]] = R.refid[e.x & ~kVar];  // normalised last loop: var left
-          R.apos[off[1]] = opos;
-          off[1] += 1;
-        } else {
-          const unsigned long long k = r_normalise(R, e);
-          R.beq[0][off[2]] = e;
-          R.bkey[0][off[2]] = k;
-          R.bpos[0][off[2]] = opos;
-          off[2] += 1;
+    for (uint32_t i0 = lo; i0 < hi; i0 += kRB) {
+      uint2 ev[kRB];
+      uint8_t fv[kRB];
+      uint4 av[kRB], bv[kRB];
+      unsigned long long kv[kRB];
+#pragma unroll
+      for (uint32_t k = 0; k < kRB; ++k) {
+        ev[k] = i0 + k < hi ? E[i0 + k] : make_uint2(kVar, kVar);
+        fv[k] = i0 + k < hi ? F[i0 + k] : 0;
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < kRB; ++k) {
+        const bool act = !r_is_var(ev[k].x) && !r_is_var(ev[k].y);
+        av[k] = act ? d.agents[ev[k].x] : make_uint4(0, 0, 0, 0);
+        bv[k] = act ? d.agents[ev[k].y] : make_uint4(0, 0, 0, 0);
+        // a parked single keeps its key (normalised last loop: var left)
+        kv[k] = !act && fv[k] && i0 + k < hi ? R.refid[ev[k].x & ~kVar] : 0ull;
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < kRB; ++k) {
+        const uint32_t i = i0 + k;
+        if (i >= hi) continue;
+        uint2 e = ev[k];
+        const uint32_t opos = i * kRPos;
+        if (r_is_var(e.x) || r_is_var(e.y)) {
+          if (fv[k]) {
+            R.aeq[off[1]] = e;
+            R.akey[off[1]] = kv[k];
+            R.apos[off[1]] = opos;
+            off[1] += 1;
+          } else {
+            const unsigned long long key = r_normalise(R, e);
+            R.beq[0][off[2]] = e;
+            R.bkey[0][off[2]] = key;
+            R.bpos[0][off[2]] = opos;
+            off[2] += 1;
+          }
+          continue;
         }
-        continue;
-      }
-      RRewrite w;
-      w.l = e.x;
-      w.r = e.y;
-      w.A = d.agents[e.x];
-      w.B = d.agents[e.y];
-      const uint32_t t = pair[w.A.x * sh.n_labels + w.B.x];
-      if (t & 1u) {  // orient as the rule's pattern (core.py:287-298)
-        const uint4 tmp = w.A;
-        w.A = w.B;
-        w.B = tmp;
-        w.l = e.y;
-        w.r = e.x;
-      }
+        RRewrite w;
+        w.l = e.x;
+        w.r = e.y;
+        w.A = av[k];
+        w.B = bv[k];
+        const uint32_t t = pair[w.A.x * sh.n_labels + w.B.x];
+        if (t & 1u) {  // orient as the rule's pattern (core.py:287-298)
+          const uint4 tmp = w.A;
+          w.A = w.B;
+          w.B = tmp;
+          w.l = e.y;
+          w.r = e.x;
+        }
 #if INET_COUNT_RULES
-      if (d.rule_hist) atomicAdd(&d.rule_hist[t >> 1], 1u);
+        if (d.rule_hist) atomicAdd(&d.rule_hist[t >> 1], 1u);
 #endif
-      const uint32_t* Rr = rules + (t >> 1) * kRuleWords;
-      const uint32_t hdr = Rr[0];
-      const uint32_t nn = hdr & 0xFFu, ne = (hdr >> 8) & 0xFFu, nf = (hdr >> 16) & 0xFFu;
-      for (uint32_t j = 0; j < nf; ++j) {  // fresh ids: base + i * max_fresh + j (engine.py:93)
-        const uint32_t q = off[5] + j;
-        const uint32_t x = q < av_v ? R.vring[(lo_v + q) & vmask] : var_bump + (q - av_v);
-        R.refid[x] = base + static_cast<unsigned long long>(i) * max_fresh + j;
-        w.fresh[j] = kVar | x;
-      }
-      off[5] += nf;
-      for (uint32_t m = 2; m < nn; ++m) {
-        const uint32_t q = off[3] + (m - 2);
-        w.extra[m - 2] = q < av_a ? R.aring[(lo_a + q) & amask] : agent_bump + (q - av_a);
-        if (sh.validate) R.alive[w.extra[m - 2]] = 1;
-      }
-      off[3] += nn > 2 ? nn - 2 : 0;
-      for (uint32_t m = 0; m < nn; ++m) {
-        const uint32_t tw = Rr[1 + m];
-        d.agents[w.src(kEnvNew + m)] =
-            make_uint4(tw & 0xFFu, w.src((tw >> 8) & 0xFFu), w.src((tw >> 16) & 0xFFu), w.src(tw >> 24));
-      }
-      for (uint32_t m = nn; m < 2; ++m) {  // consumed agents not reused in place
-        const uint32_t a = m == 0 ? w.l : w.r;
-        R.aring[(hi_a + off[4]) & amask] = a;
-        off[4] += 1;
-        if (sh.validate) R.alive[a] = 0;
-      }
-      for (uint32_t q = 0; q < ne; ++q) {
-        const uint32_t h = (Rr[9 + (q >> 1)] >> ((q & 1) * 16)) & 0xFFFFu;
-        uint2 o = make_uint2(w.src(h & 0xFFu), w.src(h >> 8));
-        if (!r_is_var(o.x) && !r_is_var(o.y)) {
-          En[off[0]] = o;
-          off[0] += 1;
-        } else {
-          const unsigned long long k = r_normalise(R, o);
-          R.beq[0][off[2]] = o;
-          R.bkey[0][off[2]] = k;
-          R.bpos[0][off[2]] = opos + q;
-          off[2] += 1;
+        const uint32_t* Rr = rules + (t >> 1) * kRuleWords;
+        const uint32_t hdr = Rr[0];
+        const uint32_t nn = hdr & 0xFFu, ne = (hdr >> 8) & 0xFFu, nf = (hdr >> 16) & 0xFFu;
+        for (uint32_t j = 0; j < nf; ++j) {  // fresh ids: base + i * max_fresh + j (engine.py:93)
+          const uint32_t q = off[5] + j;
+          const uint32_t x = q < av_v ? R.vring[(lo_v + q) & vmask] : var_bump + (q - av_v);
+          R.refid[x] = base + static_cast<unsigned long long>(i) * max_fresh + j;
+          w.fresh[j] = kVar | x;
+        }
+        off[5] += nf;
+        for (uint32_t m = 2; m < nn; ++m) {
+          const uint32_t q = off[3] + (m - 2);
+          w.extra[m - 2] = q < av_a ? R.aring[(lo_a + q) & amask] : agent_bump + (q - av_a);
+          if (sh.validate) R.alive[w.extra[m - 2]] = 1;
+        }
+        off[3] += nn > 2 ? nn - 2 : 0;
+        for (uint32_t m = 0; m < nn; ++m) {
+          const uint32_t tw = Rr[1 + m];
+          d.agents[w.src(kEnvNew + m)] =
+              make_uint4(tw & 0xFFu, w.src((tw >> 8) & 0xFFu), w.src((tw >> 16) & 0xFFu), w.src(tw >> 24));
+        }
+        for (uint32_t m = nn; m < 2; ++m) {  // consumed agents not reused in place
+          const uint32_t a = m == 0 ? w.l : w.r;
+          R.aring[(hi_a + off[4]) & amask] = a;
+          off[4] += 1;
+          if (sh.validate) R.alive[a] = 0;
+        }
+        for (uint32_t q = 0; q < ne; ++q) {
+          const uint32_t h = (Rr[9 + (q >> 1)] >> ((q & 1) * 16)) & 0xFFFFu;
+          uint2 o = make_uint2(w.src(h & 0xFFu), w.src(h >> 8));
+          if (!r_is_var(o.x) && !r_is_var(o.y)) {
+            En[off[0]] = o;
+            off[0] += 1;
+          } else {
+            const unsigned long long key = r_normalise(R, o);
+            R.beq[0][off[2]] = o;
+            R.bkey[0][off[2]] = key;
+            R.bpos[0][off[2]] = opos + q;
+            off[2] += 1;
+          }
         }
       }
     }
@@ -589,11 +637,24 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
     __syncthreads();
     const uint32_t nS = nA + nB;
     chunk_of(nS, lo, hi);
+    // this chunk's keys and their neighbours, loaded once (a run of equal keys is
+    // at most a few long: a neighbour past the window is read directly)
+    unsigned long long kw[kRW + 2];
+#pragma unroll
+    for (uint32_t k = 0; k < kRW + 2; ++k) {
+      const uint32_t p = lo + k - 1;  // kw[k] = skey[lo - 1 + k]
+      kw[k] = (lo + k >= 1 && p < nS && lo + k <= hi + 1 && k < kRW + 2) ? R.skey[p] : ~0ull;
+    }
+    const uint32_t n_kw = min(kRW + 2, hi - lo + 2);  // kw[0, n_kw) hold skey[lo - 1, lo - 1 + n_kw)
+    auto key_at = [&](uint32_t p) -> unsigned long long {
+      const uint32_t k = p + 1 - lo;
+      return p + 1 >= lo && k < n_kw ? kw[k] : R.skey[p];
+    };
     uint32_t c2[2] = {0, 0};  // 0 runs, 1 variables freed
     for (uint32_t p = lo; p < hi; ++p)
-      if (p == 0 || R.skey[p - 1] != R.skey[p]) {
+      if (p == 0 || key_at(p - 1) != key_at(p)) {
         c2[0] += 1;
-        c2[1] += p + 1 < nS && R.skey[p + 1] == R.skey[p];
+        c2[1] += p + 1 < nS && key_at(p + 1) == key_at(p);
       }
     uint32_t t2[2];
     block_scan_k<2>(c2, t2, S.scan);
@@ -603,9 +664,9 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       break;
     }
     for (uint32_t p = lo; p < hi; ++p) {
-      if (p != 0 && R.skey[p - 1] == R.skey[p]) continue;
+      if (p != 0 && key_at(p - 1) == key_at(p)) continue;
       uint32_t q = p + 1;
-      while (q < nS && R.skey[q] == R.skey[p]) ++q;
+      while (q < nS && key_at(q) == key_at(p)) ++q;
       const uint32_t out = nP + c2[0];
       c2[0] += 1;
       if (q - p == 1) {

@@ -1,6 +1,7 @@
-# GPU suite + batch / single-net timings (development loop)
-timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
-python tools/e2e_split.py 2>&1 | tail -2
-for w in fib18 a38; do echo "$w: $(python tools/profile_run.py --workload $w --repeat 3 | tail -1 | cut -c1-90)"; done
-python tools/text_speed.py 2>&1 | grep lsystem
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('bench', d['value']/1e9, d['ms_per_step'], d['e2e']['value']/1e9); print({k:(round(v['device_ms'],3),v['tier']) for k,v in d['single_nets'].items()})"
+#!/bin/bash
+# quick check: tier R tests + order timing
+T=${1:-q}
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_ordered.py tests/test_fuzz.py -q -x -m gpu > gpurun_out/${T}_ordered.txt 2>&1
+timeout 300 python tools/order_timing.py > gpurun_out/${T}_order_timing.txt 2>&1
+tail -3 gpurun_out/${T}_ordered.txt; cat gpurun_out/${T}_order_timing.txt

@@ -13,12 +13,12 @@ for name, params in (("fibonacci", (18,)), ("fibonacci", (15,)), ("addition", (3
     ctx.load_rules(prep.blob)
     ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
     row = []
-    for ordered in (False, True):
-        k = engine.native_cfg(EngineConfig(collect_stats=False), ordered=ordered)
+    for ordered, threads in ((False, 0), (True, 256), (True, 512), (True, 1024)):
+        k = engine.native_cfg(EngineConfig(collect_stats=False, threads=threads), ordered=ordered)
         code, _ = ctx.reduce(k)
         st = ctx.stats(0)
         ms = min(ctx.rerun(k) for _ in range(5))
-        row.append(f"{'R' if ordered else 'fast'}: {ms:.3f} ms, {st.rounds} loops, {st.interactions} ints, "
+        row.append(f"{'R' if ordered else 'fast'}{threads or ''}: {ms:.3f} ms, {st.rounds} loops, {st.interactions} ints, "
                    f"{st.communications} comms, {1000 * ms / max(st.rounds, 1):.2f} us/loop, tier {st.tier}")
     print(f"{name}{params}: " + " | ".join(row), flush=True)
     ctx.close()
