@@ -37,7 +37,7 @@ from .errors import (
     NoRuleForPair,
     SlotOverflow,
 )
-from .flat import FlatNet, Labels, compile_rules, flatten, is_var, term_classes, unflatten
+from .flat import FlatNet, Labels, compile_rules, flatten, flatten_many, is_var, term_classes, unflatten
 
 Configuration, Equation, RuleSet, Term = _core.Configuration, _core.Equation, _core.RuleSet, _core.Term
 iter_vars = _core.iter_vars
@@ -157,22 +157,10 @@ _blob_cache: dict = {}
 def prepare(configs: Sequence[Configuration], rules: RuleSet) -> Prepared:
     """Flatten nets and compile the rule table (host work, no device)."""
     labels = Labels.of(rules)
-    flats = [flatten(c, labels) for c in configs]  # may add config-only symbols
-    blob = compile_rules(rules, labels)
-    cat = lambda arrs, w: (np.concatenate([a.reshape(-1, w) for a in arrs]) if arrs else np.zeros((0, w), np.uint32))
-    offs = lambda arrs: np.concatenate([[0], np.cumsum([len(a) for a in arrs])]).astype(np.uint64)
-    return Prepared(
-        labels=labels,
-        blob=blob,
-        flats=flats,
-        agents=cat([f.agents for f in flats], 4),
-        agent_off=offs([f.agents for f in flats]),
-        eqs=cat([f.eqs for f in flats], 2),
-        eq_off=offs([f.eqs for f in flats]),
-        iface=np.concatenate([f.iface for f in flats]) if flats else np.zeros(0, np.uint32),
-        iface_off=offs([f.iface for f in flats]),
-        n_vars=np.array([len(f.var_ids) for f in flats], dtype=np.uint32),
-    )
+    agents, agent_off, eqs, eq_off, iface, iface_off, n_vars, infos = flatten_many(configs, labels)
+    blob = compile_rules(rules, labels)  # after flattening: config-only symbols get labels too
+    return Prepared(labels=labels, blob=blob, flats=infos, agents=agents, agent_off=agent_off, eqs=eqs,
+                    eq_off=eq_off, iface=iface, iface_off=iface_off, n_vars=n_vars)
 
 
 def native_cfg(cfg: EngineConfig, ordered: bool = False) -> _native.Cfg:

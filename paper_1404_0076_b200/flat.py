@@ -271,6 +271,50 @@ def flatten(config, labels: Labels) -> FlatNet:
     return FlatNet(agents=ag, eqs=eq, iface=fc, var_ids=var_ids, fresh_base=max_id + 1)
 
 
+@dataclass
+class FlatInfo:
+    """What unflatten needs of a flattened net (FlatNet without the arrays)."""
+
+    var_ids: list
+    fresh_base: int
+
+
+try:  # native term walks (csrc/hostpy.cpp); the Python ones below are the fallback
+    from . import _hostpy
+except ImportError:  # pragma: no cover - the extension is built with the library
+    _hostpy = None
+
+
+def flatten_many(configs, labels: Labels):
+    """Flatten a batch: (agents, agent_off, eqs, eq_off, iface, iface_off, n_vars, infos).
+
+    Same layout and numbering as ``flatten`` per net, concatenated; the native
+    walk handles the reference's classes, anything it cannot (a symbol the
+    label table lacks, arity > 3) takes the Python path.
+    """
+    configs = list(configs)
+    if _hostpy is not None and configs:
+        try:
+            ag, ao, eq, eo, fc, fo, nv, vids, fb = _hostpy.flatten_batch(
+                configs, labels.index, _core.Var, _core.Agent, _core.Symbol)
+        except LookupError:
+            pass
+        else:
+            u32 = lambda b: np.frombuffer(b, dtype=np.uint32)
+            u64 = lambda b: np.frombuffer(b, dtype=np.uint64)
+            infos = [FlatInfo(v, f) for v, f in zip(vids, fb)]
+            return (u32(ag).reshape(-1, 4), u64(ao), u32(eq).reshape(-1, 2), u64(eo), u32(fc), u64(fo), u32(nv),
+                    infos)
+    flats = [flatten(c, labels) for c in configs]
+    cat = lambda arrs, w: (np.concatenate([a.reshape(-1, w) for a in arrs]) if arrs else np.zeros((0, w), np.uint32))
+    offs = lambda arrs: np.concatenate([[0], np.cumsum([len(a) for a in arrs])]).astype(np.uint64)
+    return (cat([f.agents for f in flats], 4), offs([f.agents for f in flats]), cat([f.eqs for f in flats], 2),
+            offs([f.eqs for f in flats]),
+            np.concatenate([f.iface for f in flats]) if flats else np.zeros(0, np.uint32),
+            offs([f.iface for f in flats]), np.array([len(f.var_ids) for f in flats], dtype=np.uint32),
+            [FlatInfo(f.var_ids, f.fresh_base) for f in flats])
+
+
 def term_classes(config):
     """(Var, Agent, Equation, Configuration) classes of the caller's objects."""
     mod = sys.modules.get(type(config).__module__)
@@ -279,10 +323,14 @@ def term_classes(config):
     return _core.Var, _core.Agent, _core.Equation, _core.Configuration
 
 
-def unflatten(agents: np.ndarray, iface: np.ndarray, eqs: np.ndarray, labels: Labels, flat: FlatNet,
-              classes) -> object:
+def unflatten(agents: np.ndarray, iface: np.ndarray, eqs: np.ndarray, labels: Labels, flat, classes) -> object:
     """Device normal form (preorder agents) -> Configuration of ``classes``."""
     Var, Agent, Equation, Configuration = classes
+    if _hostpy is not None:
+        return _hostpy.unflatten(np.ascontiguousarray(agents, dtype=np.uint32).tobytes(),
+                                 np.ascontiguousarray(iface, dtype=np.uint32).tobytes(),
+                                 np.ascontiguousarray(eqs, dtype=np.uint32).tobytes(),
+                                 labels.symbols, flat.var_ids, flat.fresh_base, Var, Agent, Equation, Configuration)
     n_in = len(flat.var_ids)
     var_ids = flat.var_ids
     base = flat.fresh_base

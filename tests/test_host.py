@@ -232,3 +232,56 @@ def test_install_rebinds_reference_and_accepts_its_objects():
         b = engine.prepare([ours.build_input(*params)], ours.rules)
         for field in ("blob", "agents", "eqs", "iface", "n_vars"):
             assert np.array_equal(getattr(a, field), getattr(b, field)), (name, field)
+
+
+# -- native term walks (csrc/hostpy.cpp) against the Python ones -------------
+
+
+def test_native_flatten_and_unflatten_match_python():
+    import random
+
+    import fuzz_gen as F
+    from paper_1404_0076_b200 import engine
+
+    assert flat._hostpy is not None, "the native host extension was not built"
+    rng = random.Random(5)
+    syms = F.random_signature(rng, 6)
+    rules = F.random_rules(rng, syms)
+    nets = [F.random_net(rng, syms, rng.randint(1, 40), rng.randint(1, 6)) for _ in range(60)]
+    nets += [to_config(c["net"]) for c in ARITH[:40]]
+    rules_a = to_rules(PROGRAMS["arith"])
+    for batch, rs in ((nets[:60], rules), (nets[60:], rules_a)):
+        native = engine.prepare(batch, rs)
+        saved, flat._hostpy = flat._hostpy, None
+        try:
+            python = engine.prepare(batch, rs)
+        finally:
+            flat._hostpy = saved
+        for a in ("agents", "agent_off", "eqs", "eq_off", "iface", "iface_off", "n_vars", "blob"):
+            assert np.array_equal(getattr(native, a), getattr(python, a)), a
+        assert [(f.var_ids, f.fresh_base) for f in native.flats] == [(f.var_ids, f.fresh_base) for f in python.flats]
+        # rebuild every input from its own flat form, both ways
+        for i, cfg in enumerate(batch):
+            a0, a1 = int(native.agent_off[i]), int(native.agent_off[i + 1])
+            e0, e1 = int(native.eq_off[i]), int(native.eq_off[i + 1])
+            f0, f1 = int(native.iface_off[i]), int(native.iface_off[i + 1])
+            ag = native.agents[a0:a1]
+            # preorder-like layout: the flattener numbers parents before children
+            args = (ag, native.iface[f0:f1], native.eqs[e0:e1], native.labels, native.flats[i], flat.term_classes(cfg))
+            got = flat.unflatten(*args)
+            saved, flat._hostpy = flat._hostpy, None
+            try:
+                want = flat.unflatten(*args)
+            finally:
+                flat._hostpy = saved
+            assert got == want
+            assert print_configuration(got) == print_configuration(cfg)
+
+
+def test_native_flatten_falls_back_for_symbols_outside_the_rules():
+    from paper_1404_0076_b200 import engine
+
+    rules = parse_program("A >< B => ;\nnet : A = B;").rules
+    cfg = Configuration((Var(0),), (Equation(Var(0), Agent(Symbol("Q", 0))),))
+    prep = engine.prepare([cfg], rules)
+    assert "Q" in prep.labels.index
