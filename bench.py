@@ -23,7 +23,6 @@ from __future__ import annotations
 
 import argparse
 import concurrent.futures as cf
-import hashlib
 import json
 import os
 import statistics
@@ -319,7 +318,7 @@ def nat_text(height: int) -> str:
 
 def timed_outcomes(ctx, prep, n_nets: int, height: int) -> list:
     """(interactions, text sha prefix) of every net of the last launch, each text checked."""
-    from paper_1404_0076_b200 import engine
+    from paper_1404_0076_b200 import engine, shard
 
     ctx.finalize(0xFFFFFFFF, 0)
     tab = engine.label_table(prep.labels)
@@ -328,7 +327,7 @@ def timed_outcomes(ctx, prep, n_nets: int, height: int) -> list:
     for i in range(n_nets):
         text = ctx.text(i, tab)
         assert text == want, (i, text[:80])
-        out.append((int(ctx.stats(i).interactions), hashlib.sha256(text.encode()).hexdigest()[:16]))
+        out.append(shard.outcome(ctx.stats(i).interactions, text))
     return out
 
 
@@ -447,9 +446,9 @@ def run_ours(args) -> None:
     # final result gather: per-net (interactions, text sha) to rank 0
     gathered = shard.gather_outcomes(outcomes, world)
     if rank == 0:
-        want_sha = hashlib.sha256(nat_text(height).encode()).hexdigest()[:16]
+        want = shard.outcome(per_net, nat_text(height))
         assert len(gathered) == (BATCH_NETS if args.workload == "batch" else 1)
-        assert all(o == (per_net, want_sha) for o in gathered), "gathered outcomes differ"
+        assert all(o == want for o in gathered), "gathered outcomes differ"
 
     peak, peak_kind = load_peaks()
     achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9

@@ -48,6 +48,15 @@ def sum_over_ranks(values: Sequence[float], device="cpu") -> list[float]:
     return [float(v) for v in t.tolist()]
 
 
+def outcome(interactions: int, text: str) -> tuple:
+    """A net's gathered outcome: its interaction count and the sha256 prefix of
+    its printed normal form (print_configuration, lang.py:371-396) — 24 bytes
+    that let rank 0 check every net of every shard."""
+    import hashlib
+
+    return int(interactions), hashlib.sha256(text.encode()).hexdigest()[:16]
+
+
 def gather_outcomes(local: list, world: int) -> list:
     """All ranks' per-net outcome lists concatenated in rank (= input) order."""
     import torch.distributed as dist

@@ -38,12 +38,14 @@ def _worker(rank, world, port, n_nets, out):
         rules = O.rules_for("ackermann")
         params = [(2, k % 4) for k in range(n_nets)]
         local = []
+        texts = []
         for m, n in params[lo:hi]:
             r = O.run_config(prog.build_input(m, n), rules, collect=False)
-            local.append((m, n, r.interactions, r.printed()))
+            local.append(shard.outcome(r.interactions, r.printed()))  # bench.py's gathered format
+            texts.append((m, n, r.printed()))
         t = shard.max_over_ranks(float(rank + 1))
-        tot = shard.sum_over_ranks([sum(x[2] for x in local), len(local)])
-        allv = shard.gather_outcomes(local, world)
+        tot = shard.sum_over_ranks([sum(x[0] for x in local), len(local)])
+        allv = list(zip(shard.gather_outcomes(texts, world), shard.gather_outcomes(local, world)))
         if rank == 0:
             out.put((t, tot, allv))
     finally:
@@ -79,9 +81,11 @@ def test_two_rank_gloo_shard_and_gather():
         assert p.exitcode == 0
     assert t == 2.0  # max over ranks
     assert tot[1] == n_nets
-    assert [(m, n) for m, n, _, _ in allv] == [(2, k % 4) for k in range(n_nets)]
+    assert [(m, n) for (m, n, _), _ in allv] == [(2, k % 4) for k in range(n_nets)]
     from inet.bench import ackermann_value
+    from paper_1404_0076_b200 import shard
 
-    for m, n, ints, text in allv:
+    for (m, n, text), (ints, sha) in allv:
         assert text.count("S(") == ackermann_value(m, n)
-    assert tot[0] == sum(x[2] for x in allv)
+        assert (ints, sha) == shard.outcome(ints, text)
+    assert tot[0] == sum(o[0] for _, o in allv)
