@@ -224,6 +224,15 @@ int inet_batch_finalize(inet_ctx* ctx, uint32_t net, uint32_t n_threads);
  * load/reduce/finalize on this context. Agents are in preorder (children
  * after parents), refs are local to these arrays; variable ids are the
  * device's (input ids 0..n_vars-1 are preserved, fresh ids >= n_vars). */
+/* Whole-batch forms of inet_batch_stats / the result sizes / inet_batch_print
+ * (one call instead of one per net). inet_batch_print_all prints every
+ * finalized net with n_threads host threads (0 = all cores): a first call with
+ * buf = NULL returns the total length in *len; the second writes the texts
+ * back to back with offsets[n_nets + 1] delimiting them. */
+int inet_batch_stats_all(inet_ctx* ctx, inet_net_stats* out, uint32_t n_nets);
+int inet_batch_result_counts(inet_ctx* ctx, uint32_t* n_agents, uint32_t* n_iface, uint32_t* n_eqs, uint32_t n_nets);
+int inet_batch_print_all(inet_ctx* ctx, const char* const* names, const uint8_t* arity, uint32_t n_labels,
+                         uint32_t n_threads, char* buf, size_t cap, uint64_t* offsets, size_t* len);
 int inet_batch_result(inet_ctx* ctx, uint32_t net, const uint32_t** agents, uint32_t* n_agents,
                       const uint32_t** iface, uint32_t* n_iface, const uint32_t** eqs, uint32_t* n_eqs);
 

@@ -34,6 +34,9 @@ EXPORTS = (
     "inet_batch_reduce",
     "inet_batch_rerun",
     "inet_batch_collect",
+    "inet_batch_stats_all",
+    "inet_batch_result_counts",
+    "inet_batch_print_all",
     "inet_batch_stats",
     "inet_batch_rule_counts",
     "inet_batch_io_bytes",
@@ -115,6 +118,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             "inet_batch_reduce": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
             "inet_batch_rerun": (C.c_int, [C.c_void_p, C.POINTER(Cfg), C.POINTER(C.c_float)]),
             "inet_batch_collect": (C.c_int, [C.c_void_p]),
+            "inet_batch_stats_all": (C.c_int, [C.c_void_p, C.POINTER(NetStats), C.c_uint32]),
+            "inet_batch_result_counts": (C.c_int, [C.c_void_p, _u32p, _u32p, _u32p, C.c_uint32]),
+            "inet_batch_print_all": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.POINTER(C.c_uint8), C.c_uint32,
+                                               C.c_uint32, C.c_char_p, C.c_size_t, _u64p,
+                                               C.POINTER(C.c_size_t)]),
             "inet_batch_stats": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(NetStats)]),
             "inet_batch_totals": (C.c_int, [C.c_void_p, _u64p, _u64p, _u32p, _u32p]),
             "inet_batch_rule_counts": (C.c_int, [C.c_void_p, C.c_uint32, _u64p, C.c_uint32]),
@@ -244,6 +252,33 @@ class Context:
         code = self.lib.inet_batch_collect(self.h)
         _check(code, "batch_collect")
         return code
+
+    def stats_all(self, n: int) -> list:
+        """Every net's NetStats in one call."""
+        arr = (NetStats * max(n, 1))()
+        _check(self.lib.inet_batch_stats_all(self.h, arr, n), "batch_stats_all")
+        return list(arr)[:n]
+
+    def result_counts_all(self, n: int) -> np.ndarray:
+        """(n, 3) agents / interface terms / equations of every finalized net's normal form."""
+        out = np.zeros((3, max(n, 1)), dtype=np.uint32)
+        _check(self.lib.inet_batch_result_counts(self.h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), n),
+               "batch_result_counts")
+        return out[:, :n].T
+
+    def texts(self, n: int, labels: "LabelTable", threads: int = 0) -> list:
+        """Canonical text of every finalized net (printed natively, in parallel)."""
+        names, arity, nl = labels.args()
+        size = C.c_size_t()
+        _check(self.lib.inet_batch_print_all(self.h, names, arity, nl, threads, None, 0, None, C.byref(size)),
+               "batch_print_all")
+        buf = C.create_string_buffer(max(size.value, 1))
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        _check(self.lib.inet_batch_print_all(self.h, names, arity, nl, threads, buf, size.value,
+                                             _ptr(offs, C.c_uint64), C.byref(size)), "batch_print_all")
+        raw = buf.raw[: size.value].decode()
+        o = offs.tolist()
+        return [raw[o[i]:o[i + 1]] for i in range(n)]
 
     def stats(self, net: int) -> NetStats:
         s = NetStats()

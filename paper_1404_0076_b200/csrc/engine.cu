@@ -240,6 +240,7 @@ struct inet_ctx {
   std::vector<uint32_t> dev_rows;  // per net: device-finalized normal-form agents + 1 (0: host finalize)
   uint32_t text_net = INET_NONE;   // inet_batch_print: the net whose text is cached
   std::string text;
+  std::vector<std::string> texts;  // inet_batch_print_all: every net's text (kept for the second call)
   bool exact_code = true;  // rule-set kernel variant with reference-loop (deferred equation) code
 };
 
@@ -971,6 +972,7 @@ int finish_run(inet_ctx* c, bool fetch) {
   }
   c->reduced = true;
   c->text_net = INET_NONE;
+  c->texts.clear();
   c->results.assign(c->n_nets, inethost::NormalForm{});
   c->finalized.assign(c->n_nets, 0);
   if (fetch) {
@@ -1278,6 +1280,77 @@ int inet_batch_print(inet_ctx* c, uint32_t net, const char* const* names, const 
       c->text_net = net;
     }
     return inethost::copy_text(c->text, buf, cap, len);
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
+}
+
+int inet_batch_stats_all(inet_ctx* c, inet_net_stats* out, uint32_t n) {
+  try {
+    if (!c || !out) return INET_ERR_ARG;
+    if (!c->reduced) return INET_ERR_STATE;
+    if (n != c->n_nets) return INET_ERR_ARG;
+    std::memcpy(out, c->stats.data(), size_t(n) * sizeof(inet_net_stats));
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
+}
+
+int inet_batch_result_counts(inet_ctx* c, uint32_t* n_agents, uint32_t* n_iface, uint32_t* n_eqs, uint32_t n) {
+  try {
+    if (!c) return INET_ERR_ARG;
+    if (!c->reduced) return INET_ERR_STATE;
+    if (n != c->n_nets) return INET_ERR_ARG;
+    for (uint32_t i = 0; i < n; ++i) {
+      const bool ok = c->finalized[i] != 0;
+      const inethost::NormalForm& nf = c->results[i];
+      if (n_agents) n_agents[i] = ok ? nf.n_agents() : 0u;
+      if (n_iface) n_iface[i] = ok ? static_cast<uint32_t>(nf.iface.size()) : 0u;
+      if (n_eqs) n_eqs[i] = ok ? static_cast<uint32_t>(nf.eqs.size() / 2) : 0u;
+    }
+    return INET_OK;
+  } catch (const std::bad_alloc&) {
+    return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
+  } catch (...) {
+    return INET_ERR_ARG;
+  }
+}
+
+int inet_batch_print_all(inet_ctx* c, const char* const* names, const uint8_t* arity, uint32_t n_labels,
+                         uint32_t n_threads, char* buf, size_t cap, uint64_t* offsets, size_t* len) {
+  try {
+    if (!c || !len || (n_labels && (!names || !arity))) return INET_ERR_ARG;
+    if (!c->reduced) return INET_ERR_STATE;
+    if (!buf || c->texts.size() != c->n_nets) {
+      // print every finalized net (in parallel over host threads); failed nets print empty
+      c->texts.assign(c->n_nets, std::string());
+      const int st = inethost::parallel_for(c->n_nets, n_threads, [&](uint32_t i) -> int {
+        if (!c->finalized[i]) return INET_OK;
+        const inethost::NormalForm& nf = c->results[i];
+        return inethost::print_flat(nf.agent_data(), nf.n_agents(), nf.iface.data(), static_cast<uint32_t>(nf.iface.size()),
+                                    nf.eqs.data(), static_cast<uint32_t>(nf.eqs.size() / 2), names, arity, n_labels,
+                                    c->texts[i]);
+      });
+      if (st) return st;
+    }
+    size_t total = 0;
+    for (const auto& t : c->texts) total += t.size();
+    *len = total;
+    if (!buf || cap < total) return INET_OK;  // size query: call again with a buffer of *len bytes
+    size_t pos = 0;
+    for (uint32_t i = 0; i < c->n_nets; ++i) {
+      if (offsets) offsets[i] = pos;
+      std::memcpy(buf + pos, c->texts[i].data(), c->texts[i].size());
+      pos += c->texts[i].size();
+    }
+    if (offsets) offsets[c->n_nets] = pos;
+    c->texts.clear();
+    return INET_OK;
   } catch (const std::bad_alloc&) {
     return INET_ERR_ARENA;  // host allocation failed: reported, never thrown across the C ABI
   } catch (...) {

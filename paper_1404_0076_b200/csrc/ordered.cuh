@@ -346,6 +346,24 @@ __device__ void r_check_names(const NetDesc& d, const RArrays& R, RShared& S, co
   __syncthreads();
 }
 
+#ifdef INET_RTIMING
+// Development build: clock64 per phase of a tier R loop, thread 0's view
+// (after each phase's barrier), summed into the rule-histogram area
+// (tools/rtier_timing.py).
+#define RT_MARK(k)                       \
+  do {                                   \
+    if (threadIdx.x == 0) {              \
+      const long long _t = clock64();    \
+      rt[k] += _t - rt_last;             \
+      rt_last = _t;                      \
+    }                                    \
+  } while (0)
+#else
+#define RT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 // Reduce one net in the reference's order (see the file comment).
 __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_t* pair, const uint32_t* rules,
                                 uint32_t* hist, RShared& S) {
@@ -377,6 +395,9 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
   uint32_t loop = 0;
   unsigned long long t_prev = gt0;
   const uint32_t max_fresh = sh.max_fresh;
+#ifdef INET_RTIMING
+  long long rt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, rt_last = clock64();
+#endif
   while (!err) {
     loop += 1;
     if (loop > sh.max_rounds) {  // engine.py:205-207, before every loop
@@ -464,6 +485,7 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       err_b = d.agents[e.y].x;
       break;
     }
+    RT_MARK(0);
     const uint32_t nP = tot[0], nA = tot[1], nB = tot[2], n_act = tot[6];
     const uint32_t av_a = hi_a - lo_a, av_v = hi_v - lo_v;
     const uint32_t bump_a = tot[3] > av_a ? tot[3] - av_a : 0u, bump_v = tot[5] > av_v ? tot[5] - av_v : 0u;
@@ -571,6 +593,7 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       }
     }
     __syncthreads();
+    RT_MARK(1);
     base += static_cast<unsigned long long>(nE) * max_fresh;  // reserve(len(eqs) * max_fresh), engine.py:122
     agent_bump += bump_a;
     var_bump += bump_v;
@@ -602,6 +625,7 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       bp = R.bpos[sb];
       be = R.beq[sb];
     }
+    RT_MARK(2);
     // merge path: thread t merges its chunk of A with the B items that sort
     // before the chunk's end (A is sorted from the last loop, keys unique)
     chunk_of(nA, lo, hi);
@@ -635,6 +659,7 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       }
     }
     __syncthreads();
+    RT_MARK(3);
     const uint32_t nS = nA + nB;
     chunk_of(nS, lo, hi);
     // this chunk's keys and their neighbours, loaded once (a run of equal keys is
@@ -682,6 +707,7 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
     }
     for (uint32_t i = threadIdx.x; i < nP; i += T) Fn[i] = 0;
     __syncthreads();
+    RT_MARK(4);
     hi_v += t2[1];
     const uint32_t comms = nS - runs;
     nE = nP + runs;
@@ -702,8 +728,14 @@ __device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_
       d.stats[loop - 1] = make_uint4(n_act, comms, nE, static_cast<uint32_t>(min(now - t_prev, 0xFFFFFFFFull)));
       t_prev = now;
     }
+    RT_MARK(5);
     if (n_act == 0 && comms == 0) break;  // engine.py:222-223
   }
+#ifdef INET_RTIMING
+  if (threadIdx.x == 0 && d.rule_hist)
+    for (int k = 0; k < 8; ++k)
+      atomicAdd(reinterpret_cast<unsigned long long*>(d.rule_hist) + 32 + k, static_cast<unsigned long long>(rt[k]));
+#endif
   __syncthreads();
   // ---- results: the final list is the residual input of finalize, in order
   const bool fits = nE <= V;

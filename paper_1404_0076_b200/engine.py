@@ -241,7 +241,7 @@ def _reduce(ctx: _native.Context, prep: Prepared, cfg, ordered: bool, want_array
     """One launch over the prepared nets; per-net outcomes (results of the nets that succeeded)."""
     _code, ms = run_prepared(ctx, prep, cfg, ordered)
     n = len(prep.flats)
-    outs = [_NetOut(ctx.stats(i)) for i in range(n)]
+    outs = [_NetOut(st) for st in ctx.stats_all(n)]
     ok = [o.stats.status == _native.OK for o in outs]
     if want_arrays or want_text:
         if all(ok):
@@ -250,15 +250,16 @@ def _reduce(ctx: _native.Context, prep: Prepared, cfg, ordered: bool, want_array
             for i in range(n):
                 if ok[i]:
                     ctx.finalize(i, 1)
-        tab = label_table(prep.labels) if want_text else None
+        counts = ctx.result_counts_all(n)
+        texts = ctx.texts(n, label_table(prep.labels), finalize_threads) if want_text else None
         for i in range(n):
             if not ok[i]:
                 continue
-            outs[i].n_eqs = ctx.result_counts(i)[2]
+            outs[i].n_eqs = int(counts[i, 2])
             if want_arrays:
                 outs[i].arrays = ctx.result(i)
             if want_text:
-                outs[i].text = ctx.text(i, tab)
+                outs[i].text = texts[i]
     if cfg.collect_stats:
         for i in range(n):
             if ok[i]:
