@@ -179,6 +179,7 @@ struct GridState {
   Ctl ctl;
   RoundCtr ctr3[3];
   uint32_t bar_count, bar_gen;
+  uint32_t fin_lo_a, fin_hi_a;  // the agent ring window at the end (its entries are the dead agents)
   uint32_t blk_res[1];  // per-block residual counts follow (gridDim.x words)
 };
 
@@ -2278,6 +2279,10 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
     o->parked_total = static_cast<uint32_t>(parked_tot);
     o->pad[0] = clock_mhz(clk0, gt0);
     if ((ctl->agent_bump > d.cap_agents || ctl->var_bump > d.cap_vars) && o->err == 0) o->err = INET_ERR_ARENA;
+    o->pad[1] = 0;  // (set by the host after a device-side finalize)
+    o->pad[2] = 0;
+    g->fin_lo_a = lo_a;  // for the device-side finalize (finalize.cuh)
+    g->fin_hi_a = hi_a;
   }
 }
 

@@ -17,6 +17,7 @@
 #include "../../include/inet_b200.h"
 #include "device.cuh"
 #include "ordered.cuh"
+#include "finalize.cuh"
 #include "host.h"
 #include "jit.h"
 
@@ -190,7 +191,7 @@ struct inet_ctx {
   bool input_resident = false;
   // device state
   DevBuf d_in_agents, d_in_eqs, d_in_iface, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist,
-      d_defer, d_gs, d_rbuf;
+      d_defer, d_gs, d_rbuf, d_fin;
   bool grid_tier = false;  // the next layout is for tier X (global rings + grid state)
   bool ordered_tier = false;  // the next layout is for tier R (list and stream arrays)
   uint32_t cap_list = 0, cap_out = 0;  // tier R: equations per list / per output stream
@@ -321,7 +322,7 @@ void inet_ctx_destroy(inet_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->d_blob, &c->d_in_agents, &c->d_in_eqs, &c->d_desc, &c->d_agents, &c->d_vslot, &c->d_aring,
-                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer, &c->d_gs, &c->d_rbuf})
+                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer, &c->d_gs, &c->d_rbuf, &c->d_fin})
     b->release();
   for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -685,6 +686,82 @@ uint32_t rows_cap(const inet_ctx* c, uint32_t max_loops) {
 int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch);
 int finish_run(inet_ctx* c, bool fetch);
 
+// Tier X: finalize the net on the device (finalize.cuh). On success the
+// preorder records replace the arena prefix and the resolved interface goes
+// to residual[k].x — the layout tier S's device finalize leaves — and the
+// control block says so (pad[1] = records + 1, pad[2] = interface terms);
+// otherwise nothing changes and the host finalizes from the arena.
+int device_finalize_x(inet_ctx* c) {
+  NetCtl& k = c->ctl[0];
+  const uint32_t n = std::min(k.agent_bump, c->cap_agents), nv = std::min(k.var_bump, c->cap_vars);
+  const uint32_t m = k.n_residual, ni = static_cast<uint32_t>(c->iface_off[1] - c->iface_off[0]);
+  if (n == 0 || n >= (1u << 29) || ni == 0 || ni > 4096 || m > c->cap_vars) return INET_OK;
+  uint32_t lohi[2];
+  CUDA_TRY(cudaMemcpyAsync(lohi, static_cast<const char*>(c->d_gs.p) + offsetof(inetdev::GridState, fin_lo_a), 8,
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t E = 2 * size_t(n);
+  const size_t bytes = al(size_t(nv) * 4) * 2 + al(size_t(n) * 4) * 2 + al(size_t(n) * 16) * 2 + al(ni * 4) * 2 +
+                       al(E * 8) * 2 + 256;
+  if (c->d_fin.ensure(bytes)) return INET_ERR_CUDA;
+  uint8_t* p = static_cast<uint8_t*>(c->d_fin.p);
+  auto take = [&](size_t b) {
+    uint8_t* q = p;
+    p += al(b);
+    return q;
+  };
+  inetfin::FinArgs f{};
+  f.agents = static_cast<const uint4*>(c->d_agents.p);
+  f.n = n;
+  f.resid = static_cast<const uint2*>(c->d_resid.p);
+  f.m = m;
+  f.iface = static_cast<const uint32_t*>(c->d_in_iface.p);
+  f.ni = ni;
+  f.nv = nv;
+  f.ring = static_cast<const uint32_t*>(c->d_aring.p);
+  f.ring_mask = c->shape.ring_a - 1;
+  f.lo = lohi[0];
+  f.hi = lohi[1];
+  f.val = reinterpret_cast<uint32_t*>(take(size_t(nv) * 4));
+  f.used = reinterpret_cast<uint32_t*>(take(size_t(nv) * 4));
+  f.dead = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
+  f.parent = reinterpret_cast<uint32_t*>(take(size_t(n) * 4));
+  f.res = reinterpret_cast<uint4*>(take(size_t(n) * 16));
+  f.out = reinterpret_cast<uint4*>(take(size_t(n) * 16));
+  f.res_iface = reinterpret_cast<uint32_t*>(take(ni * 4));
+  f.out_iface = reinterpret_cast<uint32_t*>(take(ni * 4));
+  f.rk[0] = reinterpret_cast<unsigned long long*>(take(E * 8));
+  f.rk[1] = reinterpret_cast<unsigned long long*>(take(E * 8));
+  f.flag = reinterpret_cast<uint32_t*>(take(16));
+  CUDA_TRY(cudaMemsetAsync(f.flag, 0, 8, c->stream));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const dim3 grid(static_cast<uint32_t>(sms) * 8), block(256);
+  inetfin::fin_init<<<grid, block, 0, c->stream>>>(f);
+  inetfin::fin_mark<<<grid, block, 0, c->stream>>>(f);
+  inetfin::fin_resolve<<<grid, block, 0, c->stream>>>(f);
+  inetfin::fin_unused<<<grid, block, 0, c->stream>>>(f);
+  inetfin::fin_tour<<<grid, block, 0, c->stream>>>(f);
+  int cur = 0;
+  for (size_t span = 1; span < E; span *= 2) {  // ceil(log2 E) pointer-jumping steps
+    inetfin::fin_jump<<<grid, block, 0, c->stream>>>(f.rk[cur], f.rk[cur ^ 1], static_cast<uint32_t>(E));
+    cur ^= 1;
+  }
+  inetfin::fin_write<<<grid, block, 0, c->stream>>>(f, f.rk[cur]);
+  CUDA_TRY(cudaGetLastError());
+  uint32_t flag[2];
+  CUDA_TRY(cudaMemcpyAsync(flag, f.flag, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (flag[0]) return INET_OK;  // not a forest: the host finalizes
+  const uint32_t total = flag[1];
+  CUDA_TRY(cudaMemcpyAsync(c->d_agents.p, f.out, size_t(total) * 16, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(cudaMemcpy2DAsync(c->d_resid.p, 8, f.out_iface, 4, 4, ni, cudaMemcpyDeviceToDevice, c->stream));
+  k.pad[1] = total + 1;
+  k.pad[2] = ni;
+  return INET_OK;
+}
+
 int run(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   if (!c) return INET_ERR_STATE;
   c->rows_hint = 0;
@@ -939,6 +1016,10 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   }
   if (c->promoted && c->tier != kTierC) c->promoted = false;  // the cluster fell through: no prefix
   if (device_ms) *device_ms = ms + (c->promoted ? c->promo_ms : 0.0f);
+  if (fetch && c->dev_final && c->tier == inetdev::kTierX && c->n_nets == 1 && c->ctl[0].err == 0) {
+    const int st = device_finalize_x(c);
+    if (st) return st;
+  }
   return finish_run(c, fetch);
 }
 
@@ -950,7 +1031,7 @@ int finish_run(inet_ctx* c, bool fetch) {
   int first = INET_OK;
   for (uint32_t i = 0; i < c->n_nets; ++i) {
     const NetCtl& k = c->ctl[i];
-    if (c->tier == kTierS && k.err == 0) c->dev_rows[i] = k.pad[1];
+    if ((c->tier == kTierS || c->tier == inetdev::kTierX) && k.err == 0) c->dev_rows[i] = k.pad[1];
     inet_net_stats& s = c->stats[i];
     s.interactions = k.interactions;
     s.communications = k.communications;

@@ -30,9 +30,9 @@ def _ctx(dev_final):
             os.environ["INET_B200_DEVFINAL"] = old
 
 
-def _reduce(ctx, nets, rules):
+def _reduce(ctx, nets, rules, cfg=None):
     prep = engine.prepare(nets, rules)
-    code, _ = engine.run_prepared(ctx, prep, EngineConfig(collect_stats=False))
+    code, _ = engine.run_prepared(ctx, prep, cfg or EngineConfig(collect_stats=False))
     assert code == _native.OK
     assert ctx.finalize(0xFFFFFFFF, 0) == _native.OK
     out = []
@@ -150,3 +150,50 @@ def test_host_walk_equals_general_finalize_on_single_nets(name, params):
         ctx.close()
     (_, aw, iw, ew), (_, ah, ih, eh) = walk[0], ref[0]
     assert np.array_equal(aw, ah) and np.array_equal(iw, ih) and np.array_equal(ew, eh)
+
+
+@pytest.mark.parametrize("n", [12, 18, 22, 26])
+def test_whole_gpu_tier_finalized_on_device(n):
+    """Tier X nets are finalized on the device (finalize.cuh: parallel resolution,
+    Euler tour, pointer-jumping list ranking): the preorder records and the
+    interface equal the host finalize's, array for array."""
+    prog = programs.program("lsystem")
+    nets = [prog.build_input(n)]
+    cfg = EngineConfig(collect_stats=False, ctas_per_net=148)
+    dev, host = _ctx(True), _ctx(False)
+    try:
+        prep, got = _reduce(dev, nets, prog.rules, cfg)
+        _, ref = _reduce(host, nets, prog.rules, cfg)
+    finally:
+        dev.close()
+        host.close()
+    (sd, ad, idf, ed), (sh, ah, ih, eh) = got[0], ref[0]
+    assert sd.tier == _native.TIER_X and sd.device_final == 1 and sh.device_final == 0
+    assert np.array_equal(ad, ah) and np.array_equal(idf, ih) and np.array_equal(ed, eh)
+    final = unflatten(ad, idf, ed, prep.labels, prep.flats[0], engine.term_classes(nets[0]))
+    assert programs.census(final.interface[0]) == programs.lsystem_census(n)
+
+
+def test_whole_gpu_tier_device_finalize_falls_back_on_cycles():
+    """Random rule sets leave cyclic normal forms: the device finalize declines
+    them and the host's result is the oracle's net."""
+    import fuzz_gen as F
+    from netgraph import canonical
+
+    rng = random.Random(1003)
+    syms = F.random_signature(rng)
+    rules = F.random_rules(rng, syms)
+    orules = O.compile_golden_rules(F.to_golden(rules))
+    cfg = EngineConfig(collect_stats=False, ctas_per_net=148, reference_order=False)
+    ctx = _ctx(True)
+    try:
+        for _ in range(12):
+            net = F.random_net(rng, syms, rng.randint(1, 40), rng.randint(1, 6))
+            prep, got = _reduce(ctx, [net], rules, cfg)
+            st, a, i, e = got[0]
+            final = unflatten(a, i, e, prep.labels, prep.flats[0], engine.term_classes(net))
+            want = O.run_config(net, orules, collect=False)
+            assert st.interactions == want.interactions
+            assert canonical(final) == canonical(want.final_config())
+    finally:
+        ctx.close()
