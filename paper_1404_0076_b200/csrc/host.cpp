@@ -23,6 +23,7 @@
 #include <cstring>
 #include <string>
 #include <thread>
+#include <sched.h>
 #include <unordered_map>
 
 namespace inethost {
@@ -371,8 +372,19 @@ int finalize_net(const NetView& v, NormalForm& out) {
   return INET_OK;
 }
 
+// Cores this process may run on (the affinity mask, not the machine's count:
+// a container pinned to 16 of 224 cores must not spawn 224 threads).
+uint32_t usable_cores() {
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, CPU_COUNT(&set));
+  return std::max(1u, std::thread::hardware_concurrency());
+}
+
 int parallel_for(uint32_t n, uint32_t n_threads, const std::function<int(uint32_t)>& fn) {
-  if (n_threads == 0) n_threads = std::max(1u, std::thread::hardware_concurrency());
+  static const uint32_t cores = usable_cores();
+  if (n_threads == 0) n_threads = cores;
+  n_threads = std::min(n_threads, std::max(1u, n / 16));  // at least 16 items per thread
   n_threads = std::min(n_threads, n);
   std::atomic<uint32_t> next{0};
   std::atomic<int> first{INET_OK};
