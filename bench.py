@@ -258,6 +258,42 @@ def cpu_sample(program_name: str, params, seconds: float, threads: int) -> dict:
     return {"value": sum(ints) / wall, "nets": sum(done), "wall_s": wall, "interactions": sum(ints)}
 
 
+def _py_reference_net(params):
+    """One net through the reference's own Python reducer (baseline/_ref), in a worker process."""
+    sys.path.append(os.path.join(ROOT, "baseline", "_ref"))
+    from inet.bench import program
+    from inet.engine import EngineConfig, evaluate
+
+    prog = program("ackermann")
+    t0 = time.perf_counter()
+    r = evaluate(prog.build_input(*params), prog.rules, EngineConfig(collect_stats=False))
+    return r.total_interactions, time.perf_counter() - t0
+
+
+def python_reference_sample(seconds: float, threads: int, params=(3, 5)) -> dict:
+    """The unmodified Python reference (inet.engine.evaluate from baseline/_ref) on all host
+    cores, one net per process (multiprocessing, as BASELINE.md §2 plans), for ~seconds."""
+    import multiprocessing as mp
+
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "inet")):
+        return {"unavailable": "baseline/_ref not installed"}
+    ctx = mp.get_context("spawn")
+    ints, nets = 0, 0
+    t0 = time.perf_counter()
+    with ctx.Pool(threads) as pool:
+        pending = [pool.apply_async(_py_reference_net, (params,)) for _ in range(threads)]
+        while pending:
+            r = pending.pop(0).get()
+            ints += r[0]
+            nets += 1
+            if time.perf_counter() - t0 < seconds:
+                pending.append(pool.apply_async(_py_reference_net, (params,)))
+    wall = time.perf_counter() - t0
+    return {"value": ints / wall, "unit": "interactions/s", "cores": threads, "kind": "reference",
+            "sample": f"{nets} nets of ackermann{params} in {wall:.1f}s through inet.engine.evaluate "
+                      f"(the unmodified Python reference, baseline/_ref), one net per process"}
+
+
 def run_reference(args) -> None:
     rank, _, world = dist_env()
     if rank != 0:
@@ -294,10 +330,15 @@ def run_reference(args) -> None:
             "kind": "port",
             "sample": f"{sum(s['nets'] for s in per_step)} nets of {name}{params} over {args.steps} steps of "
                       f"~{args.ref_seconds}s, oracle/inet_oracle.cpp (C++ restatement of "
-                      f"inet.engine.evaluate), one net per host thread",
+                      f"inet.engine.evaluate), one net per host thread; a rate measured on a bounded sample "
+                      f"of the workload (each step a slice of the {wl.get('nets', 1)} nets), not a full pass",
+            "extrapolated": "rate over the sampled nets; every net of the workload is identical",
         },
         "e2e": {"value": value, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_python_reference:
+        # the reference's own Python reducer beside the C++ port
+        line["python_reference"] = python_reference_sample(args.py_ref_seconds, threads)
     print(json.dumps(line), flush=True)
 
 
@@ -570,6 +611,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-python-reference", action="store_true")
+    ap.add_argument("--py-ref-seconds", type=float, default=15.0)
     ap.add_argument("--no-single", dest="single", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
