@@ -560,16 +560,21 @@ def run_ours(args) -> None:
                               "agent_hw": st.agent_hw, "var_hw": st.var_hw,
                               "interactions_per_s": golden / (ms / 1000.0),
                               "us_per_round": 1000.0 * ms / max(st.rounds, 1)}
-            if engine.order_sensitive(p.rules, [p.build_input(*pparams)]):
-                # what evaluate() runs by default for this net: tier R, the reference's order
-                kr = engine.native_cfg(EngineConfig(collect_stats=False), ordered=True)
-                code, _ = c2.reduce(kr)
-                st_r = c2.stats(0)
-                assert code == _native.OK and st_r.interactions == golden
-                ms_r = min(c2.rerun(kr) for _ in range(3))
-                singles[label]["reference_order"] = {
-                    "device_ms": ms_r, "rounds": st_r.rounds, "communications": int(st_r.communications),
-                    "interactions_per_s": golden / (ms_r / 1000.0), "us_per_loop": 1000.0 * ms_r / max(st_r.rounds, 1)}
+            mode, _ = engine._plan(EngineConfig(collect_stats=False), p.rules, [p.build_input(*pparams)])
+            if mode != engine.MODE_FAST:
+                # what evaluate() runs by default for this net (reference-exact counts), and tier R
+                for key, kr in (("default_path", engine.native_cfg(EngineConfig(collect_stats=False),
+                                                                   mode == engine.MODE_R, mode == engine.MODE_STAMPS)),
+                                ("reference_order", engine.native_cfg(EngineConfig(collect_stats=False), True))):
+                    code, _ = c2.reduce(kr)
+                    st_r = c2.stats(0)
+                    assert code == _native.OK and st_r.interactions == golden
+                    ms_r = min(c2.rerun(kr) for _ in range(3))
+                    singles[label][key] = {
+                        "device_ms": ms_r, "rounds": st_r.rounds, "communications": int(st_r.communications),
+                        "tier": "SMGCXR"[st_r.tier], "interactions_per_s": golden / (ms_r / 1000.0),
+                        "us_per_loop": 1000.0 * ms_r / max(st_r.rounds, 1)}
+                singles[label]["default_path"]["mode"] = mode
             # end to end through the public API (default evaluation order), host objects in, text out
             e2e = []
             for _ in range(3):

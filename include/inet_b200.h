@@ -79,8 +79,11 @@ enum inet_status {
   INET_ERR_UNSUPPORTED = 6,  /* exceeds a device-engine limit */
   INET_ERR_NO_DEVICE = 7,    /* no CUDA device visible */
   INET_ERR_STATE = 8,        /* call order violated (e.g. fetch before reduce) */
-  INET_ERR_NAME = 9          /* NameDisciplineError       engine.py:169-183 (validate_phases); the
+  INET_ERR_NAME = 9,         /* NameDisciplineError       engine.py:169-183 (validate_phases); the
                                 variable's reference id in err_label_a (low) / err_label_b (high) */
+  INET_ERR_ORDER = 10        /* var_order: two variables made in one loop by different interactions met
+                                in a var = var equation; only the reference's list order (tier R,
+                                reference_order = 1) decides which keys it */
 };
 
 typedef struct inet_ctx inet_ctx;
@@ -106,6 +109,9 @@ typedef struct inet_cfg {
                                exactly as engine.py:106-166); 0: the fast tiers */
   uint32_t validate_phases; /* 1: name discipline checked after both phases of every loop
                                (engine.py:210-214); implies reference_order */
+  uint32_t var_order;       /* 1: the fast single-CTA tiers key var = var equations by the reference's
+                               variable ids (per-variable stamps: loop, creating interaction, bound
+                               index); INET_ERR_ORDER when that does not decide */
 } inet_cfg;
 
 /* Per-net outcome. */

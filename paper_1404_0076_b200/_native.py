@@ -18,7 +18,7 @@ from .errors import DeviceError
 LIB_PATH = os.environ.get("INET_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                              "libinetb200.so")
 
-OK, NO_RULE, LOOP_CAP, ARENA, CUDA, ARG, UNSUPPORTED, NO_DEVICE, STATE, NAME = range(10)
+OK, NO_RULE, LOOP_CAP, ARENA, CUDA, ARG, UNSUPPORTED, NO_DEVICE, STATE, NAME, ORDER = range(11)
 
 EXPORTS = (
     "inet_ctx_create",
@@ -63,6 +63,7 @@ class Cfg(C.Structure):
         ("exact_loops", C.c_uint32),
         ("reference_order", C.c_uint32),
         ("validate_phases", C.c_uint32),
+        ("var_order", C.c_uint32),
     ]
 
 
@@ -170,7 +171,7 @@ def _ptr(a: np.ndarray, ctype=C.c_uint32):
 
 
 def _check(code: int, what: str) -> None:
-    if code not in (OK, NO_RULE, LOOP_CAP, ARENA, NAME):
+    if code not in (OK, NO_RULE, LOOP_CAP, ARENA, NAME, ORDER):
         raise DeviceError(code, f"{what}: {strerror(code)}")
 
 
@@ -409,12 +410,13 @@ def jit_compile(blob: np.ndarray, tier: int = 1, threads: int = 1024) -> tuple[i
 TIER_S, TIER_M, TIER_G, TIER_C, TIER_X, TIER_R = 0, 1, 2, 3, 4, 5
 
 
-def jit_precompile(blob: np.ndarray, tier: int, threads: int, exact_code: bool, count_rules: bool) -> tuple[int, str]:
+def jit_precompile(blob: np.ndarray, tier: int, threads: int, exact_code: bool, count_rules: bool,
+                   stamps: bool = False) -> tuple[int, str]:
     """Compile one kernel variant into the package's kernels/ directory (build time)."""
     lib = load_library()
     blob = np.ascontiguousarray(blob, dtype=np.uint32)
     log = C.create_string_buffer(1 << 16)
-    flags = (1 if exact_code else 0) | (2 if count_rules else 0)
+    flags = (1 if exact_code else 0) | (2 if count_rules else 0) | (4 if stamps else 0)
     code = lib.inet_jit_precompile(_ptr(blob), blob.size, tier, threads, flags, log, len(log))
     return code, log.value.decode(errors="replace")
 

@@ -59,6 +59,12 @@
 #ifndef INET_EXACT_CODE
 #define INET_EXACT_CODE 1
 #endif
+// Reference-ordered var = var keys (single-CTA tiers): every variable carries
+// a 64-bit stamp {loop of creation, creating interaction, bound-variable
+// index}; the rule-set kernels are built with or without the code.
+#ifndef INET_STAMPS
+#define INET_STAMPS 1
+#endif
 
 namespace inetdev {
 
@@ -217,6 +223,8 @@ struct NetDesc {
   // tier R (ordered.cuh): the per-net buffer of its list and stream arrays
   uint8_t* rbuf;
   uint32_t cap_list, cap_out;
+  // reference-ordered var = var keys: one stamp per variable id (null: off)
+  unsigned long long* stamps;
 };
 
 // Launch-wide shape: ring sizes and the shared-memory capacities.
@@ -309,6 +317,8 @@ struct Round {
   uint32_t ints, comms;
   int32_t parked;
   bool failed;
+  unsigned long long* stamps;       // reference-ordered var = var keys (null: off)
+  uint32_t round, cid;              // the running round; the interaction being rewritten (its A agent)
 #ifdef INET_TIMING
   long long tm[8];
   long long tlast;
@@ -635,12 +645,44 @@ __device__ __forceinline__ void warp_push(Round<kTier>& c, bool pu, uint32_t l, 
     static_cast<uint2*>(c.out)[p] = make_uint2(l, r);
 }
 
-// Key and parked value of a non-active equation: var=var keys on the smaller id.
-__device__ __forceinline__ void key_of(uint32_t l, uint32_t r, uint32_t& key, uint32_t& val) {
+// A variable's stamp: {round of creation : 24 | creating interaction : 32 |
+// bound-variable index : 8}; input variables {0 | dense id | 0}. The
+// reference numbers fresh variables base_L + i * max_fresh + j (engine.py:93,
+// 122): by loop, then list position of the creating equation, then j. Stamps
+// decide every comparison except two variables made in the same round by
+// different interactions, whose order is their creators' list positions —
+// that case stops the net with INET_ERR_ORDER and the host reruns it on tier R.
+constexpr uint32_t kOrderUndecided = INET_ERR_ORDER;
+
+template <int kTier>
+__device__ __forceinline__ void stamp_fresh(const Round<kTier>& c, uint32_t x, uint32_t j) {
+#if INET_STAMPS
+  if (c.stamps)
+    c.stamps[x & ~vtag<kTier>()] =
+        (static_cast<unsigned long long>(c.round) << 40) | (static_cast<unsigned long long>(c.cid) << 8) | j;
+#endif
+}
+
+// Key and parked value of a non-active equation: var=var keys on the smaller
+// id (engine.py:150-153) — with stamps, the smaller reference id.
+template <int kTier>
+__device__ __forceinline__ void key_of(Round<kTier>& c, uint32_t l, uint32_t r, uint32_t& key, uint32_t& val) {
   const bool lv = (l & kVar) != 0, rv = (r & kVar) != 0;
   if (lv && rv) {
-    key = l < r ? l : r;
-    val = l < r ? r : l;
+    bool l_first = l < r;
+#if INET_STAMPS
+    if (c.stamps) {
+      const unsigned long long a = c.stamps[l & ~vtag<kTier>()], b = c.stamps[r & ~vtag<kTier>()];
+      const unsigned long long la = a >> 40, lb = b >> 40;
+      if (la != lb || la == 0 || (a >> 8) == (b >> 8)) {
+        l_first = a < b;
+      } else {
+        fail(c, kOrderUndecided, 0, 0);  // same round, different creators: tier R decides
+      }
+    }
+#endif
+    key = l_first ? l : r;
+    val = l_first ? r : l;
   } else if (lv) {
     key = l;
     val = r;
@@ -684,7 +726,7 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
     c.cur->vh = 1u;  // noted; a run that wants reference loops restarts with the full kernel
 #endif
     uint32_t key;
-    key_of(l, r, key, val);
+    key_of(c, l, r, key, val);
     x = key & ~vtag<kTier>();
     old = exch_slot(c, x, val);
   }
@@ -697,7 +739,7 @@ __device__ __forceinline__ void link(Round<kTier>& c, uint32_t l, uint32_t r) {
     return;
   }
   uint32_t key, val;
-  key_of(l, r, key, val);
+  key_of(c, l, r, key, val);
   const uint32_t x = key & ~vtag<kTier>();
   settle(c, x, exch_slot(c, x, val), val);
 }
@@ -710,8 +752,10 @@ __device__ __forceinline__ bool jit_alloc_vars(Round<kTier>& c, uint32_t (&f)[N]
   Claim k;
   if (!alloc_vars(c, N, k)) return false;
 #pragma unroll
-  for (uint32_t j = 0; j < N; ++j)
+  for (uint32_t j = 0; j < N; ++j) {
     f[j] = vtag<kTier>() | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
+    stamp_fresh(c, f[j], j);
+  }
   return true;
 }
 
@@ -732,8 +776,10 @@ __device__ __forceinline__ bool jit_alloc_vars_n(Round<kTier>& c, uint32_t n, ui
   if (!alloc_vars(c, n, k)) return false;
 #pragma unroll
   for (uint32_t j = 0; j < N; ++j)
-    if (j < n)
+    if (j < n) {
       f[j] = vtag<kTier>() | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
+      stamp_fresh(c, f[j], j);
+    }
   return true;
 }
 
@@ -849,6 +895,12 @@ __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uin
   for (uint32_t j = 0; j < MF; ++j) f[j] = vtag<kTier>() | (j < gv ? rv[j] : bump_var(c, bv + (j - gv)));
 #pragma unroll
   for (uint32_t j = 0; j < MX; ++j) g[j] = j < ga ? ra[j] : bump_agent(c, ba + (j - ga));
+#if INET_STAMPS
+  if (c.stamps)
+#pragma unroll
+    for (uint32_t j = 0; j < MF; ++j)
+      if (j < nf) stamp_fresh(c, f[j], j);
+#endif
   return true;
 }
 
@@ -860,7 +912,7 @@ __device__ __forceinline__ bool jit_prep(Round<kTier>& c, uint32_t l, uint32_t r
     return false;
   }
   uint32_t key;
-  key_of(l, r, key, val);
+  key_of(c, l, r, key, val);
   x = key & ~vtag<kTier>();
   return true;
 }
@@ -892,6 +944,7 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
 #if !defined(INET_CTIMING) && INET_COUNT_RULES
   if (c.d->rule_hist) atomicAdd(&c.d->rule_hist[t >> 1], 1u);
 #endif
+  c.cid = l;  // identifies this interaction in its fresh variables' stamps
 #ifdef INET_JIT
   jit_apply<kTier>(c, t >> 1, A, B, l, r);
   c.ints += 1;
@@ -912,6 +965,10 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
   auto extra = [&](uint32_t q) -> uint32_t {
     return q < na.got ? static_cast<uint32_t>(c.aring[(na.pos + q) & c.amask]) : bump_agent(c, na.bump + (q - na.got));
   };
+#if INET_STAMPS
+  if (c.stamps)
+    for (uint32_t j = 0; j < nf; ++j) stamp_fresh(c, fresh(j), j);
+#endif
   uint32_t env_l[Traits<kTier>::kEnvLocal ? kEnvSize : 1];
   if constexpr (Traits<kTier>::kEnvLocal) {
     // Small nets (tier S): a per-thread table in local memory; with several
@@ -983,7 +1040,7 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
         push_active(c, el, er);
       } else {
         uint32_t key;
-        key_of(el, er, key, vals[e]);
+        key_of(c, el, er, key, vals[e]);
         xs[e] = key & ~vtag<kTier>();
         olds[e] = exch_slot(c, xs[e], vals[e]);
       }
@@ -1262,6 +1319,14 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   }
   __syncthreads();
   c.failed = false;
+  c.stamps = INET_STAMPS ? d.stamps : nullptr;
+  c.round = 0;
+  c.cid = 0;
+#if INET_STAMPS
+  if (c.stamps)  // input variables: {round 0 | dense id}, dense ids are in the input's id order
+    for (uint32_t x = threadIdx.x; x < d.n_in_vars; x += blockDim.x) c.stamps[x] = static_cast<unsigned long long>(x) << 8;
+  __syncthreads();
+#endif
   c.env = smem + plan.env_off + threadIdx.x;
   if constexpr (T::kEnvSmem) c.env[(kEnvSize - 1) * blockDim.x] = kNone;  // (disabled tier option)
 #ifdef INET_TIMING
@@ -1285,6 +1350,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   for (uint32_t r = 1; !stop; ++r) {
     RoundCtr* cur = &ctl->ctr3[set];
     c.cur = cur;
+    c.round = r;
     c.lo_a = lo_a;
     c.hi_a = hi_a;
     c.lo_v = lo_v;
@@ -1673,6 +1739,8 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
 #endif
   cluster_barrier();
   c.failed = false;
+  c.stamps = nullptr;  // (single-CTA tiers only)
+  c.round = c.cid = 0;
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0;
   // running totals: thread 0 of CTA 0
   unsigned long long tot_i = d.base_ints, tot_c = d.base_comms, t_prev = globaltimer();
@@ -2106,6 +2174,8 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
   __shared__ uint32_t scan_scratch[34];
   grid_barrier(g);
   c.failed = false;
+  c.stamps = nullptr;  // (single-CTA tiers only)
+  c.round = c.cid = 0;
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, rounds = 1;
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();

@@ -191,7 +191,7 @@ struct inet_ctx {
   bool input_resident = false;
   // device state
   DevBuf d_in_agents, d_in_eqs, d_in_iface, d_desc, d_agents, d_vslot, d_aring, d_vring, d_queue, d_stats, d_resid, d_ctl, d_hist,
-      d_defer, d_gs, d_rbuf, d_fin;
+      d_defer, d_gs, d_rbuf, d_fin, d_stamps;
   bool grid_tier = false;  // the next layout is for tier X (global rings + grid state)
   bool ordered_tier = false;  // the next layout is for tier R (list and stream arrays)
   uint32_t cap_list = 0, cap_out = 0;  // tier R: equations per list / per output stream
@@ -243,6 +243,7 @@ struct inet_ctx {
   std::string text;
   std::vector<std::string> texts;  // inet_batch_print_all: every net's text (kept for the second call)
   bool exact_code = true;  // rule-set kernel variant with reference-loop (deferred equation) code
+  bool var_order = false;  // stamps: var = var keyed in the reference's id order (single-CTA tiers)
 };
 
 inline uint32_t hist_stride(const inet_ctx* c) { return std::max(c->n_rules, 128u); }
@@ -322,7 +323,7 @@ void inet_ctx_destroy(inet_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->d_blob, &c->d_in_agents, &c->d_in_eqs, &c->d_desc, &c->d_agents, &c->d_vslot, &c->d_aring,
-                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer, &c->d_gs, &c->d_rbuf, &c->d_fin})
+                    &c->d_vring, &c->d_queue, &c->d_stats, &c->d_resid, &c->d_ctl, &c->d_hist, &c->d_defer, &c->d_gs, &c->d_rbuf, &c->d_fin, &c->d_stamps})
     b->release();
   for (auto& kv : c->jit_kernels) cudaLibraryUnload(kv.second.first);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -448,6 +449,7 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
   const size_t r_bytes =
       c->ordered_tier ? inetdev::r_carve(nullptr, cap_agents, cap_vars, c->cap_list, c->cap_out, nullptr) : 0;
   if (c->ordered_tier && c->d_rbuf.ensure(N * r_bytes)) return INET_ERR_CUDA;
+  if (c->var_order && c->d_stamps.ensure(N * cap_vars * 8)) return INET_ERR_CUDA;
   if (c->grid_tier) CUDA_TRY(cudaMemsetAsync(c->d_gs.p, 0, sizeof(inetdev::GridState) + 4096 * 4, c->stream));
   if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * hist_stride(c) * 4, c->stream));
   std::vector<NetDesc> desc(n);
@@ -480,6 +482,7 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.in_iface = static_cast<const uint32_t*>(c->d_in_iface.p) + c->iface_off[i];
     d.n_iface = static_cast<uint32_t>(c->iface_off[i + 1] - c->iface_off[i]);
     d.dev_final = c->dev_final ? 1u : 0u;
+    if (c->var_order) d.stamps = static_cast<unsigned long long*>(c->d_stamps.p) + size_t(i) * cap_vars;
     if (c->ordered_tier) {
       d.rbuf = static_cast<uint8_t*>(c->d_rbuf.p) + size_t(i) * r_bytes;
       d.cap_list = c->cap_list;
@@ -546,11 +549,13 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
   // code style per tier: straight-line cases where the rewrite is issue-bound
   // (S, M, G); a uniform memory phase where remote latency dominates (C)
   const int style = c->jit_style >= 0 ? c->jit_style : (tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0);
-  const auto key = std::make_tuple(tier, threads, style + (c->exact_code ? 16 : 0) + (c->count_rules ? 32 : 0));
+  const auto key = std::make_tuple(tier, threads,
+                                   style + (c->exact_code ? 16 : 0) + (c->count_rules ? 32 : 0) + (c->var_order ? 64 : 0));
   auto it = c->jit_kernels.find(key);
   if (it != c->jit_kernels.end()) return reinterpret_cast<const void*>(it->second.second);
   const std::string src =
-      inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style, c->exact_code, c->count_rules);
+      inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style, c->exact_code, c->count_rules,
+                             c->var_order);
   std::vector<char> cubin;
   if (inetjit::compile_cubin(src, cubin, c->jit_log) != 0) {
     std::fprintf(stderr, "inet_b200: rule-set JIT unavailable, using the prebuilt kernels: %s\n", c->jit_log.c_str());
@@ -813,6 +818,8 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   bool with_defer = exact && !c->jit_mode;  // the prebuilt kernels always carry the code
   // Tier R: the reference's list order (ordered.cuh), capacities doubled on overflow.
   const bool ordered = cfg && (cfg->reference_order || cfg->validate_phases);
+  // stamps (reference-ordered var = var keys) run on the single-CTA tiers only
+  c->var_order = !ordered && cfg && cfg->var_order;
   if (ordered) {
     c->resume.on = false;  // a hand-over of an earlier single-net run must not leak into this layout
     c->promoted = false;
@@ -911,6 +918,7 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   // equations, rounds and totals — and a 16-CTA cluster (tier C) resumes it
   // from there, which wins once rounds are wide. 1 forces one CTA per net.
   uint32_t want_g = cfg ? cfg->ctas_per_net : 0;
+  if (c->var_order) want_g = 1;  // no cluster or whole-GPU tier: one CTA, tier M then G
   if (want_g == 0 && c->n_nets == 1 && !user_caps) {
     want_g = 16;
     if (c->max_in_agents < 32768 && c->max_in_vars < 16384) {
@@ -955,7 +963,7 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   }
   // Single nets too large for a cluster (or ctas_per_net > 16): the whole GPU
   // (tier X), capacities doubled on overflow.
-  if (!done && c->n_nets == 1 && (cfg ? cfg->ctas_per_net : 0) != 1) {
+  if (!done && c->n_nets == 1 && (cfg ? cfg->ctas_per_net : 0) != 1 && !c->var_order) {
     uint32_t ca = cfg && cfg->cap_agents ? cfg->cap_agents : (1u << 20);
     uint32_t cv = cfg && cfg->cap_vars ? cfg->cap_vars : (1u << 20);
     ca = std::max(ca, c->max_in_agents + 64);
@@ -1231,7 +1239,9 @@ int inet_jit_precompile(const uint32_t* blob, size_t n_words, int tier, uint32_t
     const int style = tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0;  // as jit_kernel picks it
     std::string msg;
     const int rc = inetjit::precompile(
-        inetjit::kernel_source(blob, n_words, tier, threads, style, (flags & 1u) != 0, (flags & 2u) != 0), msg);
+        inetjit::kernel_source(blob, n_words, tier, threads, style, (flags & 1u) != 0, (flags & 2u) != 0,
+                               (flags & 4u) != 0),
+        msg);
     if (log && log_len) {
       std::strncpy(log, msg.c_str(), log_len - 1);
       log[log_len - 1] = 0;

@@ -61,11 +61,15 @@ class EngineConfig(_ref_engine.EngineConfig):
     False links to a fixpoint within a round. ``reference_order``: True runs
     tier R, the reference's equation list in its own order (every count, row,
     error and residual equation exactly as engine.py:106-166 produces them);
-    False the fast tiers only; None (default) picks tier R for rule sets and
-    nets where the order can show (``order_sensitive``) and reruns a net on
-    tier R after a fast run that failed with NoRuleForPair or left equations in
-    its normal form. ``validate_phases`` also runs on tier R (the name
-    discipline is checked on the device after both phases of every loop).
+    False the fast tiers only; None (default) gives the reference's results
+    the fast way where it can (``_plan``): nets that can equate two variables
+    run on the single-CTA tiers with reference-ordered var = var keys
+    (per-variable stamps), rule sets with an orientation-dependent same-symbol
+    rule run on tier R, and a net whose fast run failed with NoRuleForPair,
+    met a var = var comparison the stamps cannot decide, or left equations in
+    its normal form is rerun on tier R. ``validate_phases`` also runs on tier
+    R (the name discipline is checked on the device after both phases of
+    every loop).
     """
 
     device: int = 0
@@ -163,7 +167,7 @@ def prepare(configs: Sequence[Configuration], rules: RuleSet) -> Prepared:
                     eq_off=eq_off, iface=iface, iface_off=iface_off, n_vars=n_vars)
 
 
-def native_cfg(cfg: EngineConfig, ordered: bool = False) -> _native.Cfg:
+def native_cfg(cfg: EngineConfig, ordered: bool = False, var_order: bool = False) -> _native.Cfg:
     k = _native.Cfg()
     k.max_loops = max(0, min(int(cfg.max_loops), 0xFFFFFFFE))
     k.collect_stats = 1 if cfg.collect_stats else 0
@@ -172,13 +176,15 @@ def native_cfg(cfg: EngineConfig, ordered: bool = False) -> _native.Cfg:
     k.exact_loops = 1 if getattr(cfg, "exact_loops", True) else 0
     k.reference_order = 1 if ordered else 0
     k.validate_phases = 1 if cfg.validate_phases else 0
+    k.var_order = 1 if var_order else 0
     return k
 
 
-def run_prepared(ctx: _native.Context, prep: Prepared, cfg: EngineConfig, ordered: bool = False) -> tuple[int, float]:
+def run_prepared(ctx: _native.Context, prep: Prepared, cfg: EngineConfig, ordered: bool = False,
+                 var_order: bool = False) -> tuple[int, float]:
     ctx.load_rules(prep.blob, key=prep.blob.tobytes())
     ctx.load_batch(prep.agents, prep.agent_off, prep.eqs, prep.eq_off, prep.iface, prep.iface_off, prep.n_vars)
-    return ctx.reduce(native_cfg(cfg, ordered))
+    return ctx.reduce(native_cfg(cfg, ordered, var_order))
 
 
 # ---------------------------------------------------------------------------
@@ -189,42 +195,51 @@ def _rule_equates_variables(rule) -> bool:
     return any(is_var(e.lhs) and is_var(e.rhs) for e in rule.rhs)
 
 
-def order_sensitive(rules: RuleSet, configs: Sequence[Configuration] = ()) -> bool:
-    """Can the reference's own list order show in this run's results?
-
-    Yes when a var = var equation can arise — a rule right-hand side equating
-    two variables or an input equation between variables: the reference keys it
-    on the smaller variable id (engine.py:150-153), which decides the loop of
-    the merge, total_communications and the LoopStats rows — or when a
-    same-symbol rule is not symmetric in its two agents (it is applied in the
-    orientation of the equation, core.py:287-298, which for a merged pair is
-    the list order, engine.py:161-165). Such runs go to tier R.
-    """
+def _asymmetric_same_symbol(rules: RuleSet) -> bool:
     from .flat import same_symbol_rule_is_symmetric
 
-    for rule in rules.rules.values():
-        if _rule_equates_variables(rule):
-            return True
-        if rule.lhs_a.name == rule.lhs_b.name and not same_symbol_rule_is_symmetric(rule):
-            return True
+    return any(r.lhs_a.name == r.lhs_b.name and not same_symbol_rule_is_symmetric(r) for r in rules.rules.values())
+
+
+def equates_variables(rules: RuleSet, configs: Sequence[Configuration] = ()) -> bool:
+    """Can a var = var equation arise (a rule right-hand side or an input equation
+    between two variables)? The reference keys it on the smaller variable id
+    (engine.py:150-153), which decides the loop of the merge,
+    total_communications and the LoopStats rows."""
+    if any(_rule_equates_variables(r) for r in rules.rules.values()):
+        return True
     return any(is_var(e.lhs) and is_var(e.rhs) for c in configs for e in c.equations)
 
 
-def _wants_order(cfg, rules: RuleSet, configs: Sequence[Configuration]) -> Optional[bool]:
-    """True: tier R; False: the fast tiers only; None: fast tiers with exactness reruns."""
+def order_sensitive(rules: RuleSet, configs: Sequence[Configuration] = ()) -> bool:
+    """Can the reference's own list order show in this run's results?
+
+    Yes when a var = var equation can arise (``equates_variables``) or when a
+    same-symbol rule is not symmetric in its two agents (it is applied in the
+    orientation of the equation, core.py:287-298, which for a merged pair is
+    the list order, engine.py:161-165).
+    """
+    return _asymmetric_same_symbol(rules) or equates_variables(rules, configs)
+
+
+# Evaluation modes: the reference's list on the device (tier R); the fast tiers;
+# the fast single-CTA tiers with reference-ordered var = var keys (stamps).
+MODE_R, MODE_FAST, MODE_STAMPS = "R", "fast", "stamps"
+
+
+def _plan(cfg, rules: RuleSet, configs: Sequence[Configuration]) -> tuple[str, bool]:
+    """(mode, reruns): how to reduce, and whether nets whose outcome the fast
+    tiers cannot pin to the reference's order get a second run on tier R."""
     if cfg.validate_phases:
-        return True
+        return MODE_R, False
     forced = getattr(cfg, "reference_order", None)
     if forced is not None:
-        return bool(forced)
-    if not getattr(cfg, "exact_loops", True):
-        # fixpoint linking is the device's own loop structure: only an
-        # orientation-dependent rule still needs the reference's order
-        from .flat import same_symbol_rule_is_symmetric
-
-        asym = any(r.lhs_a.name == r.lhs_b.name and not same_symbol_rule_is_symmetric(r) for r in rules.rules.values())
-        return True if asym else None
-    return True if order_sensitive(rules, configs) else None
+        return (MODE_R if forced else MODE_FAST), False
+    if _asymmetric_same_symbol(rules):
+        return MODE_R, False
+    if getattr(cfg, "exact_loops", True) and equates_variables(rules, configs):
+        return MODE_STAMPS, True
+    return MODE_FAST, True
 
 
 @dataclass
@@ -236,10 +251,10 @@ class _NetOut:
     n_eqs: int = 0
 
 
-def _reduce(ctx: _native.Context, prep: Prepared, cfg, ordered: bool, want_arrays: bool, want_text: bool,
+def _reduce(ctx: _native.Context, prep: Prepared, cfg, mode: str, want_arrays: bool, want_text: bool,
             finalize_threads: int = 0) -> tuple[list, float]:
     """One launch over the prepared nets; per-net outcomes (results of the nets that succeeded)."""
-    _code, ms = run_prepared(ctx, prep, cfg, ordered)
+    _code, ms = run_prepared(ctx, prep, cfg, mode == MODE_R, mode == MODE_STAMPS)
     n = len(prep.flats)
     outs = [_NetOut(st) for st in ctx.stats_all(n)]
     ok = [o.stats.status == _native.OK for o in outs]
@@ -271,31 +286,30 @@ def _evaluate_nets(configs: Sequence[Configuration], rules: RuleSet, cfg, want_a
                    finalize_threads: int = 0):
     """Reduce nets with the evaluation order ``cfg`` asks for; returns (prep, outs, device ms).
 
-    Fast tiers first when the order cannot matter (``_wants_order`` None), then
-    tier R for exactly the nets where the reference's list order could still
-    show: a NoRuleForPair (which pair of the loop fails first, and its
-    orientation, engine.py:88-92) and a normal form that keeps equations
-    (where finalize cuts a cycle depends on the list order, engine.py:313-355).
+    The mode ``_plan`` picks first, then (default policy) tier R for exactly
+    the nets where the reference's list order could still show: a
+    NoRuleForPair (which pair of the loop fails first, and its orientation,
+    engine.py:88-92), a var = var comparison between two variables made in one
+    loop by different interactions (INET_ERR_ORDER), and a normal form that
+    keeps equations (where finalize cuts a cycle depends on the list order,
+    engine.py:313-355).
     """
-    want = _wants_order(cfg, rules, configs)
-    if want is False:
-        from .flat import same_symbol_rule_is_symmetric
-
-        for rule in rules.rules.values():
-            if rule.lhs_a.name == rule.lhs_b.name and not same_symbol_rule_is_symmetric(rule):
-                raise UnsupportedNet(
-                    f"rule {rule.lhs_a.name}><{rule.lhs_b.name} is not symmetric in its two agents: with "
-                    "reference_order=False its result would depend on the orientation of a merged pair")
+    mode, reruns = _plan(cfg, rules, configs)
+    if mode == MODE_FAST and not reruns and _asymmetric_same_symbol(rules):
+        bad = next(r for r in rules.rules.values() if r.lhs_a.name == r.lhs_b.name)
+        raise UnsupportedNet(
+            f"rule {bad.lhs_a.name}><{bad.lhs_b.name} is not symmetric in its two agents: with "
+            "reference_order=False its result would depend on the orientation of a merged pair")
     ctx = _native.context(getattr(cfg, "device", 0))
     prep = prepare(configs, rules)
     with ctx.lock:
-        outs, ms = _reduce(ctx, prep, cfg, bool(want), want_arrays, want_text, finalize_threads)
-        if want is None:
+        outs, ms = _reduce(ctx, prep, cfg, mode, want_arrays, want_text, finalize_threads)
+        if reruns:
             redo = [i for i, o in enumerate(outs)
-                    if o.stats.status == _native.NO_RULE or o.n_eqs > 0]
+                    if o.stats.status in (_native.NO_RULE, _native.ORDER) or o.n_eqs > 0]
             if redo:
                 sub = prepare([configs[i] for i in redo], rules)
-                souts, sms = _reduce(ctx, sub, cfg, True, want_arrays, want_text, finalize_threads)
+                souts, sms = _reduce(ctx, sub, cfg, MODE_R, want_arrays, want_text, finalize_threads)
                 for j, i in enumerate(redo):
                     outs[i] = souts[j]
                     outs[i].sub = (sub, j)

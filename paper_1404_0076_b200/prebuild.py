@@ -38,12 +38,22 @@ def shipped_blobs() -> dict:
     return out
 
 
+# single-CTA variants with reference-ordered var = var keys (engine._plan: rule
+# sets that equate variables — fibonacci, addition, arith)
+STAMP_VARIANTS = [(_native.TIER_S, 128), (_native.TIER_S, 256), (_native.TIER_S, 512), (_native.TIER_M, 256),
+                  (_native.TIER_M, 512)]
+
+
 def precompile_shipped(workers: int = 8) -> list:
     jobs = []
     for name, blob in shipped_blobs().items():
         for tier, threads in VARIANTS:
             for exact in (False, True):
                 jobs.append((name, blob, tier, threads, exact, False))
+        if name in ("fibonacci", "addition", "arith"):
+            for tier, threads in STAMP_VARIANTS:
+                for exact in (False, True):
+                    jobs.append((name, blob, tier, threads, exact, False, True))
         # accounting runs of bench.py (per-rule histogram)
         if name in ("ackermann", "lsystem", "fibonacci"):
             for tier, threads in ((_native.TIER_S, 128), (_native.TIER_M, 256), (_native.TIER_C, 256),
@@ -52,8 +62,9 @@ def precompile_shipped(workers: int = 8) -> list:
     failed = []
 
     def one(job):
-        name, blob, tier, threads, exact, count = job
-        code, log = _native.jit_precompile(blob, tier, threads, exact, count)
+        name, blob, tier, threads, exact, count = job[:6]
+        stamps = len(job) > 6 and job[6]
+        code, log = _native.jit_precompile(blob, tier, threads, exact, count, stamps)
         if code != 0:
             failed.append((name, tier, threads, exact, count, log[-400:]))
 

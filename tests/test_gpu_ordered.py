@@ -88,10 +88,13 @@ def test_arith_551_nets_everything_equal():
 
 
 def test_fib18_default_is_reference_exact_and_repeatable():
-    """Fibonacci equates variables (Add >< Z => r = y), so evaluate() picks tier R:
+    """Fibonacci equates variables (Add >< Z => r = y): evaluate() keys var = var
+    equations by the reference's variable ids (stamps on tier M) and gives
     1,667 loops and 47,912 communications on every run."""
     prog = programs.program("fibonacci")
     runs = [evaluate(prog.build_input(18), prog.rules) for _ in range(3)]
+    st = _native.context(0).stats(0)
+    assert st.tier == _native.TIER_M, "the stamped fast tier, not a tier R rerun"
     for res in runs:
         assert res.total_interactions == 50_515
         assert res.total_communications == 47_912
@@ -100,6 +103,44 @@ def test_fib18_default_is_reference_exact_and_repeatable():
     assert _rows(runs[0]) == _rows(runs[1]) == _rows(runs[2])
     want = O.run_config(prog.build_input(18), O.rules_for("fibonacci"), collect=True)
     assert _rows(runs[0]) == [list(r) for r in want.rows]
+
+
+def test_stamped_fast_tiers_against_every_fixture():
+    """Single-CTA tiers with reference-ordered var = var keys: every fixture and
+    the 551 random nets equal in everything, or stopped with INET_ERR_ORDER
+    (then tier R decides, as the default policy does)."""
+    from paper_1404_0076_b200 import engine
+
+    ctx = _native.context(0)
+    undecided = 0
+    cases = [c for c in CASES if "error" not in c]
+    for case in cases:
+        config, rules = _inputs(case)
+        prep = engine.prepare([config], rules)
+        with ctx.lock:
+            outs, _ = engine._reduce(ctx, prep, EngineConfig(**case.get("engine_config", {})), engine.MODE_STAMPS,
+                                     True, True)
+        o = outs[0]
+        if o.stats.status == _native.ORDER:
+            undecided += 1
+            continue
+        assert o.stats.status == _native.OK, case["name"]
+        assert o.stats.interactions == case["interactions"], case["name"]
+        assert o.stats.communications == case["communications"], case["name"]
+        assert [list(r[:3]) for r in o.rows] == case["loops"], case["name"]
+        assert _sha(o.text) == case["print_sha256"], case["name"]
+    rules = to_rules(PROGRAMS["arith"])
+    prep = engine.prepare([to_config(c["net"]) for c in ARITH], rules)
+    with ctx.lock:
+        outs, _ = engine._reduce(ctx, prep, EngineConfig(), engine.MODE_STAMPS, False, True)
+    for case, o in zip(ARITH, outs):
+        if o.stats.status == _native.ORDER:
+            undecided += 1
+            continue
+        assert o.stats.communications == case["communications"], case["name"]
+        assert [list(r[:3]) for r in o.rows] == case["loops"], case["name"]
+        assert _sha(o.text) == case["print_sha256"], case["name"]
+    assert undecided < (len(cases) + len(ARITH)) // 4
 
 
 def test_fast_tiers_remain_available():
