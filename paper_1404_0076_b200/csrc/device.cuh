@@ -1347,6 +1347,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
   uint32_t set = 1, set_next = 2;  // r % 3 and (r + 1) % 3, rotated
+  bool in_active = false;          // this thread rewrote an input equation (round 1)
   for (uint32_t r = 1; !stop; ++r) {
     RoundCtr* cur = &ctl->ctr3[set];
     c.cur = cur;
@@ -1383,16 +1384,19 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
           const bool v = i < n && !c.failed;
           const uint2 eq = v ? make_uint2(ref_in<kTier>(d.in_eqs[i].x), ref_in<kTier>(d.in_eqs[i].y)) : make_uint2(0, 0);
           const bool act = v && ((eq.x | eq.y) & kVar) == 0;
+          in_active |= act;
           interact_w(c, act, eq.x, eq.y);
           if (v && !act && !c.failed) link(c, eq.x, eq.y);
         }
       } else {
         for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
           const uint2 eq = make_uint2(ref_in<kTier>(d.in_eqs[i].x), ref_in<kTier>(d.in_eqs[i].y));
-          if (((eq.x | eq.y) & kVar) == 0)
+          if (((eq.x | eq.y) & kVar) == 0) {
+            in_active = true;
             interact(c, eq.x, eq.y);
-          else
+          } else {
             link(c, eq.x, eq.y);
+          }
         }
       }
     } else if constexpr (T::kPacked) {
@@ -1440,7 +1444,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       }
     }
     INET_TMARK(c, 6);
-    __syncthreads();
+    const bool any_input_active = __syncthreads_or(in_active) != 0;  // (round 1: the input's active pairs)
     INET_TMARK(c, 7);
     // ---- close round r (every thread, same values)
     const RoundCtr k = *cur;
@@ -1477,7 +1481,11 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
                                     static_cast<uint32_t>(now - t_prev));
       t_prev = now;
     }
-    rounds = r + 1;
+    // a round that had no pairs and whose deferred equations all parked was
+    // itself the reference's trailing no-op loop (exact mode: the last loop can
+    // be communication only); no second trailing row then
+    const bool was_noop = (r > 1 ? n == 0 : !any_input_active) && q == 0 && (INET_EXACT_CODE ? k.dcount : 0u) == 0;
+    rounds = was_noop ? r : r + 1;
     n = q;
     nd = INET_EXACT_CODE ? k.dcount : 0u;
     if (round_failed) {
@@ -1485,6 +1493,8 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     } else if (!INET_EXACT_CODE && sh.detect_vh && k.vh) {
       stop = true;  // the host reruns the net with reference-loop code
       stop_err = kNeedExact;
+    } else if (was_noop) {
+      stop = true;  // this round was the trailing no-op loop (its row is written)
     } else if (r + 1 > sh.max_rounds) {  // engine.py:205-207 (checked before every loop, the no-op one too)
       stop = true;
       stop_err = INET_ERR_LOOP_CAP;
