@@ -944,7 +944,9 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
 #if !defined(INET_CTIMING) && INET_COUNT_RULES
   if (c.d->rule_hist) atomicAdd(&c.d->rule_hist[t >> 1], 1u);
 #endif
+#if INET_STAMPS
   c.cid = l;  // identifies this interaction in its fresh variables' stamps
+#endif
 #ifdef INET_JIT
   jit_apply<kTier>(c, t >> 1, A, B, l, r);
   c.ints += 1;
@@ -1444,7 +1446,11 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       }
     }
     INET_TMARK(c, 6);
-    const bool any_input_active = __syncthreads_or(in_active) != 0;  // (round 1: the input's active pairs)
+    bool any_input_active = false;  // round 1: were any input equations active pairs?
+    if (r == 1)
+      any_input_active = __syncthreads_or(in_active) != 0;
+    else
+      __syncthreads();
     INET_TMARK(c, 7);
     // ---- close round r (every thread, same values)
     const RoundCtr k = *cur;

@@ -6,6 +6,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_1404_0076_b200  # noqa: E402,F401  (the reference package `inet` on the path)
 import fuzz_gen as F  # noqa: E402
 from golden_io import load, to_config, to_rules  # noqa: E402
 from paper_1404_0076_b200 import EngineConfig, _native, engine  # noqa: E402
