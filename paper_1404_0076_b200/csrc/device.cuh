@@ -189,7 +189,9 @@ struct GridState {
   uint32_t blk_res[1];  // per-block residual counts follow (gridDim.x words)
 };
 
-// Per-net device view of its private global arrays.
+// Per-net device view of its private global arrays. (Pointers first, then
+// 64-bit, then 32-bit fields: no padding — every CTA keeps a copy in shared
+// memory, and tier S packs 10 CTAs per SM.)
 struct NetDesc {
   uint4* agents;       // cap_agents (tiers M/G arena; tier S result copy)
   uint32_t* vslot;     // cap_vars (tier G)
@@ -198,34 +200,31 @@ struct NetDesc {
   uint2* residual;     // cap_vars
   NetCtl* ctl;
   uint32_t* rule_hist; // interactions per rule (accounting runs) or null
-  uint32_t cap_agents, cap_vars, cap_queue, cap_rounds;
   // initial contents (device copies of the caller's flat arrays)
   const uint4* in_agents;
   const uint2* in_eqs;
-  uint32_t n_in_agents, n_in_eqs, n_in_vars, pad;
   // reference loop mode: equations a merge left var-headed wait for the next
   // round's communication, [2 parities][cap_def] (tier C: [2][G][cap_def / G])
   uint2* deferred;
-  uint32_t cap_def, pad2;
-  // tier C resuming a net that tier M handed over (its arena, slot table and
-  // pending equations are the inputs): the rounds and totals already done
-  uint32_t resume, round_base;
-  unsigned long long base_ints, base_comms;
-  int32_t base_parked;
-  uint32_t pad3;
   // tier X: global free rings and the net's global control block
   uint32_t* g_aring;
   uint32_t* g_vring;
   struct GridState* gs;
   // device-side finalize (tier S): the net's interface; dev_final enables it
   const uint32_t* in_iface;
-  uint32_t n_iface, dev_final;
-  // tier R (ordered.cuh): the per-net buffer of its list and stream arrays
-  uint8_t* rbuf;
-  uint32_t cap_list, cap_out;
   // reference-ordered var = var keys: one stamp per variable id (null: off)
   unsigned long long* stamps;
+  // tier C resuming a net that tier M handed over (its arena, slot table and
+  // pending equations are the inputs): the totals already done
+  unsigned long long base_ints, base_comms;
+  uint32_t cap_agents, cap_vars, cap_queue, cap_rounds;
+  uint32_t n_in_agents, n_in_eqs, n_in_vars;
+  uint32_t cap_def;
+  uint32_t resume, round_base;  // (tier C resume: the rounds already done)
+  int32_t base_parked;
+  uint32_t n_iface, dev_final;  // dev_final: bit 0 device-side finalize (tier S), bit 1 kInputActive
 };
+constexpr uint32_t kInputActive = 2u;  // NetDesc::dev_final: an input equation is an active pair
 
 // Launch-wide shape: ring sizes and the shared-memory capacities.
 struct Shape {
@@ -243,6 +242,9 @@ struct Shape {
                                   // kernel without INET_EXACT_CODE)
   uint32_t max_fresh;             // tier R: RuleSet.max_fresh (the reference's fresh-id block per equation)
   uint32_t validate;              // tier R: name discipline after every phase (EngineConfig.validate_phases)
+  uint32_t cap_list, cap_out;     // tier R: equations per list / per output stream
+  uint8_t* rbuf;                  // tier R: net i's arrays start at rbuf + i * rbuf_stride (ordered.cuh)
+  unsigned long long rbuf_stride;
 };
 
 // Internal statuses (never returned to callers): a single-CTA run that outgrew
@@ -317,8 +319,10 @@ struct Round {
   uint32_t ints, comms;
   int32_t parked;
   bool failed;
+#if INET_STAMPS
   unsigned long long* stamps;       // reference-ordered var = var keys (null: off)
   uint32_t round, cid;              // the running round; the interaction being rewritten (its A agent)
+#endif
 #ifdef INET_TIMING
   long long tm[8];
   long long tlast;
@@ -1321,10 +1325,10 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   }
   __syncthreads();
   c.failed = false;
-  c.stamps = INET_STAMPS ? d.stamps : nullptr;
+#if INET_STAMPS
+  c.stamps = d.stamps;
   c.round = 0;
   c.cid = 0;
-#if INET_STAMPS
   if (c.stamps)  // input variables: {round 0 | dense id}, dense ids are in the input's id order
     for (uint32_t x = threadIdx.x; x < d.n_in_vars; x += blockDim.x) c.stamps[x] = static_cast<unsigned long long>(x) << 8;
   __syncthreads();
@@ -1349,11 +1353,12 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
   uint32_t set = 1, set_next = 2;  // r % 3 and (r + 1) % 3, rotated
-  bool in_active = false;          // this thread rewrote an input equation (round 1)
   for (uint32_t r = 1; !stop; ++r) {
     RoundCtr* cur = &ctl->ctr3[set];
     c.cur = cur;
+#if INET_STAMPS
     c.round = r;
+#endif
     c.lo_a = lo_a;
     c.hi_a = hi_a;
     c.lo_v = lo_v;
@@ -1386,19 +1391,16 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
           const bool v = i < n && !c.failed;
           const uint2 eq = v ? make_uint2(ref_in<kTier>(d.in_eqs[i].x), ref_in<kTier>(d.in_eqs[i].y)) : make_uint2(0, 0);
           const bool act = v && ((eq.x | eq.y) & kVar) == 0;
-          in_active |= act;
           interact_w(c, act, eq.x, eq.y);
           if (v && !act && !c.failed) link(c, eq.x, eq.y);
         }
       } else {
         for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
           const uint2 eq = make_uint2(ref_in<kTier>(d.in_eqs[i].x), ref_in<kTier>(d.in_eqs[i].y));
-          if (((eq.x | eq.y) & kVar) == 0) {
-            in_active = true;
+          if (((eq.x | eq.y) & kVar) == 0)
             interact(c, eq.x, eq.y);
-          } else {
+          else
             link(c, eq.x, eq.y);
-          }
         }
       }
     } else if constexpr (T::kPacked) {
@@ -1446,11 +1448,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       }
     }
     INET_TMARK(c, 6);
-    bool any_input_active = false;  // round 1: were any input equations active pairs?
-    if (r == 1)
-      any_input_active = __syncthreads_or(in_active) != 0;
-    else
-      __syncthreads();
+    __syncthreads();
     INET_TMARK(c, 7);
     // ---- close round r (every thread, same values)
     const RoundCtr k = *cur;
@@ -1490,7 +1488,8 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     // a round that had no pairs and whose deferred equations all parked was
     // itself the reference's trailing no-op loop (exact mode: the last loop can
     // be communication only); no second trailing row then
-    const bool was_noop = (r > 1 ? n == 0 : !any_input_active) && q == 0 && (INET_EXACT_CODE ? k.dcount : 0u) == 0;
+    const bool was_noop = (r > 1 ? n == 0 : (d.dev_final & kInputActive) == 0) && q == 0 &&
+                          (INET_EXACT_CODE ? k.dcount : 0u) == 0;
     rounds = was_noop ? r : r + 1;
     n = q;
     nd = INET_EXACT_CODE ? k.dcount : 0u;
@@ -1570,7 +1569,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   const uint32_t ahw = min(ctl->agent_bump, c.cap_agents);
   uint32_t nf_rows = 0;  // device-finalized normal form: agents + 1 (0: the host finalizes)
   if constexpr (kTier == kTierS) {
-    if (d.dev_final && !handed) nf_rows = finalize_smem(c, d, ctl, plan, smem, sh, hw, ahw, base);
+    if ((d.dev_final & 1u) && !handed) nf_rows = finalize_smem(c, d, ctl, plan, smem, sh, hw, ahw, base);
   }
   if constexpr (T::kAgentsSmem) {
     const uint32_t n_copy = nf_rows ? 0u : min(ahw, d.cap_agents);
@@ -1755,8 +1754,10 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
 #endif
   cluster_barrier();
   c.failed = false;
+#if INET_STAMPS
   c.stamps = nullptr;  // (single-CTA tiers only)
   c.round = c.cid = 0;
+#endif
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0;
   // running totals: thread 0 of CTA 0
   unsigned long long tot_i = d.base_ints, tot_c = d.base_comms, t_prev = globaltimer();
@@ -2190,8 +2191,10 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
   __shared__ uint32_t scan_scratch[34];
   grid_barrier(g);
   c.failed = false;
+#if INET_STAMPS
   c.stamps = nullptr;  // (single-CTA tiers only)
   c.round = c.cid = 0;
+#endif
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, rounds = 1;
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();

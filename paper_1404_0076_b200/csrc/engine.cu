@@ -195,6 +195,7 @@ struct inet_ctx {
   bool grid_tier = false;  // the next layout is for tier X (global rings + grid state)
   bool ordered_tier = false;  // the next layout is for tier R (list and stream arrays)
   uint32_t cap_list = 0, cap_out = 0;  // tier R: equations per list / per output stream
+  size_t r_bytes = 0;                  // tier R: bytes of one net's arrays (layout)
   uint32_t cap_def = 0;  // deferred equations per net and round (reference loop mode)
   bool count_rules = false;
   std::vector<uint32_t> h_hist;
@@ -446,9 +447,8 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
       (c->grid_tier && (c->d_aring.ensure(size_t(cap_agents) * 4) || c->d_vring.ensure(size_t(cap_vars) * 4) ||
                         c->d_gs.ensure(sizeof(inetdev::GridState) + 4096 * 4))))
     return INET_ERR_CUDA;
-  const size_t r_bytes =
-      c->ordered_tier ? inetdev::r_carve(nullptr, cap_agents, cap_vars, c->cap_list, c->cap_out, nullptr) : 0;
-  if (c->ordered_tier && c->d_rbuf.ensure(N * r_bytes)) return INET_ERR_CUDA;
+  c->r_bytes = c->ordered_tier ? inetdev::r_carve(nullptr, cap_agents, cap_vars, c->cap_list, c->cap_out, nullptr) : 0;
+  if (c->ordered_tier && c->d_rbuf.ensure(N * c->r_bytes)) return INET_ERR_CUDA;
   if (c->var_order && c->d_stamps.ensure(N * cap_vars * 8)) return INET_ERR_CUDA;
   if (c->grid_tier) CUDA_TRY(cudaMemsetAsync(c->d_gs.p, 0, sizeof(inetdev::GridState) + 4096 * 4, c->stream));
   if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * hist_stride(c) * 4, c->stream));
@@ -482,12 +482,12 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
     d.in_iface = static_cast<const uint32_t*>(c->d_in_iface.p) + c->iface_off[i];
     d.n_iface = static_cast<uint32_t>(c->iface_off[i + 1] - c->iface_off[i]);
     d.dev_final = c->dev_final ? 1u : 0u;
+    for (uint64_t e = c->eq_off[i]; e < c->eq_off[i + 1]; ++e)  // an input active pair (round 1 is not a no-op loop)
+      if (!(c->eqs[2 * e] & INET_VAR_BIT) && !(c->eqs[2 * e + 1] & INET_VAR_BIT)) {
+        d.dev_final |= inetdev::kInputActive;
+        break;
+      }
     if (c->var_order) d.stamps = static_cast<unsigned long long*>(c->d_stamps.p) + size_t(i) * cap_vars;
-    if (c->ordered_tier) {
-      d.rbuf = static_cast<uint8_t*>(c->d_rbuf.p) + size_t(i) * r_bytes;
-      d.cap_list = c->cap_list;
-      d.cap_out = c->cap_out;
-    }
     if (c->resume.on && n == 1) {
       // resume from tier M's hand-over: its arena, slot table and pending equations
       d.in_agents = d.agents;
@@ -576,6 +576,12 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
 }
 
 int launch(inet_ctx* c, const inet_cfg* cfg, Shape sh, int tier, float* ms) {
+  if (tier == inetdev::kTierR) {
+    sh.rbuf = static_cast<uint8_t*>(c->d_rbuf.p);
+    sh.rbuf_stride = c->r_bytes;
+    sh.cap_list = c->cap_list;
+    sh.cap_out = c->cap_out;
+  }
   const uint32_t threads = tier == kTierC                ? cluster_threads(cfg)
                            : tier == inetdev::kTierX     ? 256u
                            : tier == inetdev::kTierR     ? (c->n_nets > 64 ? 256u : tier_r_threads(cfg))

@@ -365,12 +365,12 @@ __device__ void r_check_names(const NetDesc& d, const RArrays& R, RShared& S, co
 #endif
 
 // Reduce one net in the reference's order (see the file comment).
-__device__ void run_net_ordered(const NetDesc& d, const Shape& sh, const uint16_t* pair, const uint32_t* rules,
-                                uint32_t* hist, RShared& S) {
+__device__ void run_net_ordered(const NetDesc& d, const Shape& sh, uint32_t net, const uint16_t* pair,
+                                const uint32_t* rules, uint32_t* hist, RShared& S) {
   RArrays R;
-  r_carve(d.rbuf, d.cap_agents, d.cap_vars, d.cap_list, d.cap_out, &R);
+  r_carve(sh.rbuf + net * sh.rbuf_stride, d.cap_agents, d.cap_vars, sh.cap_list, sh.cap_out, &R);
   const uint32_t T = blockDim.x;
-  const uint32_t A = d.cap_agents, V = d.cap_vars, Lc = d.cap_list, Oc = d.cap_out;
+  const uint32_t A = d.cap_agents, V = d.cap_vars, Lc = sh.cap_list, Oc = sh.cap_out;
   const uint32_t amask = pow2_at_least(A) - 1, vmask = pow2_at_least(V) - 1;
   const long long clk0 = clock64();
   const unsigned long long gt0 = globaltimer();
@@ -773,7 +773,7 @@ __device__ __forceinline__ void reduce_ordered_body(const NetDesc* __restrict__ 
     __syncthreads();
     if (threadIdx.x == 0) sd = nets[net];
     __syncthreads();
-    run_net_ordered(sd, sh, pair, rules, hist, S);
+    run_net_ordered(sd, sh, net, pair, rules, hist, S);
   }
 }
 
