@@ -661,9 +661,12 @@ constexpr uint32_t kOrderUndecided = INET_ERR_ORDER;
 template <int kTier>
 __device__ __forceinline__ void stamp_fresh(const Round<kTier>& c, uint32_t x, uint32_t j) {
 #if INET_STAMPS
-  if (c.stamps)
+  if (c.stamps) {
     c.stamps[x & ~vtag<kTier>()] =
         (static_cast<unsigned long long>(c.round) << 40) | (static_cast<unsigned long long>(c.cid) << 8) | j;
+    // ordered before the exchange that may hand x to another thread this round
+    __threadfence_block();
+  }
 #endif
 }
 
@@ -676,6 +679,7 @@ __device__ __forceinline__ void key_of(Round<kTier>& c, uint32_t l, uint32_t r, 
     bool l_first = l < r;
 #if INET_STAMPS
     if (c.stamps) {
+      __threadfence_block();  // (after the exchange that delivered a variable made this round)
       const unsigned long long a = c.stamps[l & ~vtag<kTier>()], b = c.stamps[r & ~vtag<kTier>()];
       const unsigned long long la = a >> 40, lb = b >> 40;
       if (la != lb || la == 0 || (a >> 8) == (b >> 8)) {
