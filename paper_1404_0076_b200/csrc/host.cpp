@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -425,16 +426,20 @@ struct Printer {
   const uint8_t* arity;
   uint32_t nl;
   uint64_t budget;  // agents a walk may visit (a tree visits each once)
+  std::vector<uint32_t>* st;      // walk stack (per thread, reused across nets)
+  const std::vector<uint32_t>* nlen;  // strlen of every label name
 
   bool agent_ok(uint32_t a) const { return a < na && ag[4 * a] < nl; }
 
   // structural skeleton: Name( children ) with ? for variables
   bool skeleton(uint32_t root, std::string& out) {
-    std::vector<uint32_t> st{root};
+    std::vector<uint32_t>& s = *st;
+    s.clear();
+    s.push_back(root);
     uint64_t seen = 0;
-    while (!st.empty()) {
-      const uint32_t t = st.back();
-      st.pop_back();
+    while (!s.empty()) {
+      const uint32_t t = s.back();
+      s.pop_back();
       if (t == kNone - 1) {
         out.push_back(')');
         continue;
@@ -446,21 +451,23 @@ struct Printer {
       }
       if (!agent_ok(t) || ++seen > budget) return false;
       const uint32_t lab = ag[4 * t];
-      out.append(names[lab]);
+      out.append(names[lab], (*nlen)[lab]);
       out.push_back('(');
-      st.push_back(kNone - 1);
-      for (int k = int(arity[lab]) - 1; k >= 0; --k) st.push_back(ag[4 * t + 1 + k]);
+      s.push_back(kNone - 1);
+      for (int k = int(arity[lab]) - 1; k >= 0; --k) s.push_back(ag[4 * t + 1 + k]);
     }
     return true;
   }
 
   // first-occurrence variable numbering, preorder (children left to right)
   bool assign(uint32_t root, std::unordered_map<uint32_t, uint32_t>& ids) {
-    std::vector<uint32_t> st{root};
+    std::vector<uint32_t>& s = *st;
+    s.clear();
+    s.push_back(root);
     uint64_t seen = 0;
-    while (!st.empty()) {
-      const uint32_t t = st.back();
-      st.pop_back();
+    while (!s.empty()) {
+      const uint32_t t = s.back();
+      s.pop_back();
       if (t == kNone) return false;
       if (t & kVar) {
         ids.emplace(t & ~kVar, static_cast<uint32_t>(ids.size()));
@@ -468,17 +475,20 @@ struct Printer {
       }
       if (!agent_ok(t) || ++seen > budget) return false;
       const uint32_t lab = ag[4 * t];
-      for (int k = int(arity[lab]) - 1; k >= 0; --k) st.push_back(ag[4 * t + 1 + k]);
+      for (int k = int(arity[lab]) - 1; k >= 0; --k) s.push_back(ag[4 * t + 1 + k]);
     }
     return true;
   }
 
   bool term(uint32_t root, const std::unordered_map<uint32_t, uint32_t>& ids, std::string& out) {
-    std::vector<uint32_t> st{root};
+    std::vector<uint32_t>& s = *st;
+    s.clear();
+    s.push_back(root);
     uint64_t seen = 0;
-    while (!st.empty()) {
-      const uint32_t t = st.back();
-      st.pop_back();
+    char num[16];
+    while (!s.empty()) {
+      const uint32_t t = s.back();
+      s.pop_back();
       if (t == kNone - 1) {
         out.push_back(')');
         continue;
@@ -489,19 +499,20 @@ struct Printer {
       }
       if (t & kVar) {
         out.push_back('x');
-        out.append(std::to_string(ids.at(t & ~kVar)));
+        const int w = std::snprintf(num, sizeof(num), "%u", ids.at(t & ~kVar));
+        out.append(num, static_cast<size_t>(w));
         continue;
       }
       if (!agent_ok(t) || ++seen > budget) return false;
       const uint32_t lab = ag[4 * t];
-      out.append(names[lab]);
+      out.append(names[lab], (*nlen)[lab]);
       const uint32_t n = arity[lab];
       if (n == 0) continue;
       out.push_back('(');
-      st.push_back(kNone - 1);
+      s.push_back(kNone - 1);
       for (int k = int(n) - 1; k >= 0; --k) {
-        st.push_back(ag[4 * t + 1 + k]);
-        if (k) st.push_back(kNone - 2);
+        s.push_back(ag[4 * t + 1 + k]);
+        if (k) s.push_back(kNone - 2);
       }
     }
     return true;
@@ -513,9 +524,16 @@ struct Printer {
 int print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface, uint32_t n_iface,
                const uint32_t* eqs, uint32_t n_eqs, const char* const* names, const uint8_t* arity,
                uint32_t n_labels, std::string& out) {
-  for (uint32_t l = 0; l < n_labels; ++l)
+  // per-thread scratch, reused across the nets a worker prints
+  thread_local std::vector<uint32_t> stack;
+  thread_local std::vector<uint32_t> nlen;
+  thread_local std::unordered_map<uint32_t, uint32_t> ids;
+  nlen.resize(n_labels);
+  for (uint32_t l = 0; l < n_labels; ++l) {
     if (!names[l] || arity[l] > 3) return INET_ERR_ARG;
-  Printer p{agents, n_agents, names, arity, n_labels, uint64_t(n_agents) + 1};
+    nlen[l] = static_cast<uint32_t>(std::strlen(names[l]));
+  }
+  Printer p{agents, n_agents, names, arity, n_labels, uint64_t(n_agents) + 1, &stack, &nlen};
   // orientation and order of the equations
   struct Eq {
     uint32_t l, r;
@@ -534,12 +552,14 @@ int print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface,
     const int c = x.a.compare(y.a);
     return c != 0 ? c < 0 : x.b < y.b;
   });
-  std::unordered_map<uint32_t, uint32_t> ids;
+  ids.clear();
   for (uint32_t i = 0; i < n_iface; ++i)
     if (!p.assign(iface[i], ids)) return INET_ERR_ARG;
   for (const Eq& e : es)
     if (!p.assign(e.l, ids) || !p.assign(e.r, ids)) return INET_ERR_ARG;
-  out.assign("net");
+  out.clear();
+  out.reserve(size_t(n_agents) * 3 + 16);
+  out.append("net");
   if (n_iface) out.push_back(' ');
   for (uint32_t i = 0; i < n_iface; ++i) {
     if (i) out.append(", ");
