@@ -391,9 +391,12 @@ def run_ours(args) -> None:
 
     rank, local, world = dist_env()
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = local
+        # --test-one-device: every rank on GPU 0 over gloo (exercises the multi-rank
+        # path on a one-GPU box; NCCL refuses two ranks on one device)
+        dist.init_process_group("gloo" if args.test_one_device else "nccl", init_method="env://")
+    dev = 0 if args.test_one_device else local
+    torch.cuda.set_device(dev)
+    cdev = "cpu" if args.test_one_device else f"cuda:{dev}"  # where the control collectives run
     name, params, wl = workload_spec(args.workload)
     prog = program(name)
     if args.workload == "batch":
@@ -404,7 +407,7 @@ def run_ours(args) -> None:
         configs = [prog.build_input(*params)]
         per_net = SINGLE[wl["net"]][2]
     n_nets = len(configs)
-    ecfg = EngineConfig(collect_stats=False, threads=args.threads)
+    ecfg = EngineConfig(collect_stats=False, threads=args.threads, device=dev)
     prep = engine.prepare(configs, prog.rules)
     ctx = _native.Context(dev)
     ctx.load_rules(prep.blob)
@@ -450,9 +453,9 @@ def run_ours(args) -> None:
     assert nfail_t == 0 and ti_t == ti and tc_t == tc, (ti_t, tc_t, nfail_t)
     outcomes = timed_outcomes(ctx, prep, n_nets, height)
     my_ms = sum(times)
-    max_ms = shard.max_over_ranks(my_ms, device=f"cuda:{dev}")
+    max_ms = shard.max_over_ranks(my_ms, device=cdev)
     # interactions of one step, all ranks (each rank verified its own count above)
-    total_interactions = int(shard.sum_over_ranks([float(ti)], device=f"cuda:{dev}")[0])
+    total_interactions = int(shard.sum_over_ranks([float(ti)], device=cdev)[0])
     value = total_interactions * args.steps / (max_ms / 1000.0)
     kernel_ms = my_ms / args.steps
 
@@ -469,7 +472,7 @@ def run_ours(args) -> None:
         assert code == _native.OK and len(agents0) == height + 1
         h2d, d2h = ctx.io_bytes()
         assert ctx.totals()[0] == ti
-    e2e_max = shard.max_over_ranks(sum(e2e_times), device=f"cuda:{dev}")
+    e2e_max = shard.max_over_ranks(sum(e2e_times), device=cdev)
     e2e_value = total_interactions * len(e2e_times) / e2e_max
 
     # e2e through the Python API a user calls: evaluate_batch(as_text=True) on
@@ -481,7 +484,7 @@ def run_ours(args) -> None:
         out = engine.evaluate_batch(configs, prog.rules, ecfg, as_terms=False, as_text=True)
         api_times.append(time.perf_counter() - t0)
         assert out.total_interactions == ti
-    api_max = shard.max_over_ranks(min(api_times), device=f"cuda:{dev}")
+    api_max = shard.max_over_ranks(min(api_times), device=cdev)
     api_value = total_interactions / api_max
 
     # final result gather: per-net (interactions, text sha) to rank 0
@@ -617,6 +620,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-python-reference", action="store_true")
+    ap.add_argument("--test-one-device", action="store_true",
+                    help="(testing) all ranks on GPU 0 with gloo collectives")
     ap.add_argument("--py-ref-seconds", type=float, default=15.0)
     ap.add_argument("--no-single", dest="single", action="store_false")
     args = ap.parse_args()
