@@ -89,3 +89,24 @@ def test_two_rank_gloo_shard_and_gather():
         assert text.count("S(") == ackermann_value(m, n)
         assert (ints, sha) == shard.outcome(ints, text)
     assert tot[0] == sum(o[0] for _, o in allv)
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu(tmp_path):
+    """bench.py under torchrun with 2 ranks (both on GPU 0, gloo control
+    collectives): shards, max-over-ranks timing and the final gather of all
+    4096 nets' outcomes to rank 0, which checks every one."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--test-one-device", "--no-single", "--no-cpu-baseline",
+           "--api-steps", "1", "--e2e-steps", "1"]
+    proc = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    line = json.loads([l for l in proc.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["gather"]["nets"] == 4096
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
