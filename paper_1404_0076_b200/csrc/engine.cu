@@ -515,12 +515,24 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
     if (t <= 512) return 512;
     return 1024;
   }
-  // measured on 4096/1024/512/256 x A(3,6): 128 threads once there are about
-  // as many nets as SMs x 7, 256 below that; a few nets (one per SM) are
-  // round-latency bound: 256 threads (fib(18): 2.72 ms vs 3.21 ms at 1024)
-  if (c->n_nets >= 1024) return 128;
-  if (c->n_nets >= 256) return 256;
-  return c->n_nets >= 16 ? 512 : 256;
+  // measured on 2..4096 x A(3,6) (profiles/r02x_style_sweep.txt): 128 threads
+  // once there are more nets than ~3 per SM (style 0 past ~768 nets, style 1
+  // below), 256 below that; single nets 256 (fib(18): 2.72 ms vs 3.21 at 1024)
+  return c->n_nets > 400 ? 128u : 256u;
+}
+
+// Rule-code style of the rule-set kernels (jit.cpp): tier C and X fixed; tier S
+// by load — the uniform style 1 (selects, one memory phase per warp) is ~30 %
+// faster per round while few nets share an SM (latency-bound: a warp no longer
+// runs one dependent chain per rule present in it), the straight-line style 0
+// once the SMs are full (issue-bound: 36.1 vs 45.3 ms for 4096 x A(3,6));
+// profiles/r02x_style_sweep.txt.
+int tier_style(const inet_ctx* c, int tier) {
+  if (c->jit_style >= 0) return c->jit_style;
+  if (tier == kTierC) return 1;
+  if (tier == inetdev::kTierX) return 2;
+  if (tier == kTierS) return c->n_nets <= 768 ? 1 : 0;
+  return 0;
 }
 
 // CTA size of tier R for a few nets (env INET_B200_RTHREADS overrides; measured).
@@ -548,7 +560,7 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
   if (!c->jit_mode) return nullptr;
   // code style per tier: straight-line cases where the rewrite is issue-bound
   // (S, M, G); a uniform memory phase where remote latency dominates (C)
-  const int style = c->jit_style >= 0 ? c->jit_style : (tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0);
+  const int style = tier_style(c, tier);
   const auto key = std::make_tuple(tier, threads,
                                    style + (c->exact_code ? 16 : 0) + (c->count_rules ? 32 : 0) + (c->var_order ? 64 : 0));
   auto it = c->jit_kernels.find(key);
@@ -1242,7 +1254,9 @@ int inet_jit_precompile(const uint32_t* blob, size_t n_words, int tier, uint32_t
     if (!blob || n_words < 4) return INET_ERR_ARG;
     if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
     if (tier < kTierS || tier > inetdev::kTierX) return INET_ERR_ARG;
-    const int style = tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0;  // as jit_kernel picks it
+    // as jit_kernel picks it, or flags bits 8-11 = style + 1
+    const int style = (flags >> 8) & 15u ? static_cast<int>(((flags >> 8) & 15u) - 1u)
+                                         : tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0;
     std::string msg;
     const int rc = inetjit::precompile(
         inetjit::kernel_source(blob, n_words, tier, threads, style, (flags & 1u) != 0, (flags & 2u) != 0,

@@ -20,11 +20,13 @@ from ._ref import bench as _bench
 
 load_rules, program = _bench.load_rules, _bench.program
 
-# (tier, threads) the engine's tier selection uses (engine.cu auto_threads /
-# cluster_threads): batches of >= 1024, >= 256, >= 16 nets; single nets.
+# (tier, threads, style) the engine's selection uses (engine.cu auto_threads /
+# tier_style / cluster_threads): batches of > 768 nets (style 0, 128 threads),
+# 401..768 (style 1, 128), fewer (style 1, 256); single nets; -1 = the tier's
+# default style.
 VARIANTS = [
-    (_native.TIER_S, 128), (_native.TIER_S, 256), (_native.TIER_S, 512),
-    (_native.TIER_M, 256), (_native.TIER_C, 256), (_native.TIER_X, 256),
+    (_native.TIER_S, 128, 0), (_native.TIER_S, 128, 1), (_native.TIER_S, 256, 1), (_native.TIER_S, 256, 0),
+    (_native.TIER_M, 256, -1), (_native.TIER_C, 256, -1), (_native.TIER_X, 256, -1),
 ]
 
 
@@ -40,31 +42,30 @@ def shipped_blobs() -> dict:
 
 # single-CTA variants with reference-ordered var = var keys (engine._plan: rule
 # sets that equate variables — fibonacci, addition, arith)
-STAMP_VARIANTS = [(_native.TIER_S, 128), (_native.TIER_S, 256), (_native.TIER_S, 512), (_native.TIER_M, 256),
-                  (_native.TIER_M, 512)]
+STAMP_VARIANTS = [(_native.TIER_S, 128, 0), (_native.TIER_S, 128, 1), (_native.TIER_S, 256, 1),
+                  (_native.TIER_M, 256, -1)]
 
 
 def precompile_shipped(workers: int = 8) -> list:
     jobs = []
     for name, blob in shipped_blobs().items():
-        for tier, threads in VARIANTS:
+        for tier, threads, style in VARIANTS:
             for exact in (False, True):
-                jobs.append((name, blob, tier, threads, exact, False))
+                jobs.append((name, blob, tier, threads, exact, False, False, style))
         if name in ("fibonacci", "addition", "arith"):
-            for tier, threads in STAMP_VARIANTS:
+            for tier, threads, style in STAMP_VARIANTS:
                 for exact in (False, True):
-                    jobs.append((name, blob, tier, threads, exact, False, True))
+                    jobs.append((name, blob, tier, threads, exact, False, True, style))
         # accounting runs of bench.py (per-rule histogram)
         if name in ("ackermann", "lsystem", "fibonacci"):
-            for tier, threads in ((_native.TIER_S, 128), (_native.TIER_M, 256), (_native.TIER_C, 256),
-                                  (_native.TIER_X, 256)):
-                jobs.append((name, blob, tier, threads, False, True))
+            for tier, threads, style in ((_native.TIER_S, 128, 0), (_native.TIER_M, 256, -1),
+                                         (_native.TIER_C, 256, -1), (_native.TIER_X, 256, -1)):
+                jobs.append((name, blob, tier, threads, False, True, False, style))
     failed = []
 
     def one(job):
-        name, blob, tier, threads, exact, count = job[:6]
-        stamps = len(job) > 6 and job[6]
-        code, log = _native.jit_precompile(blob, tier, threads, exact, count, stamps)
+        name, blob, tier, threads, exact, count, stamps, style = job
+        code, log = _native.jit_precompile(blob, tier, threads, exact, count, stamps, style)
         if code != 0:
             failed.append((name, tier, threads, exact, count, log[-400:]))
 
