@@ -527,12 +527,16 @@ uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
 // runs one dependent chain per rule present in it), the straight-line style 0
 // once the SMs are full (issue-bound: 36.1 vs 45.3 ms for 4096 x A(3,6));
 // profiles/r02x_style_sweep.txt.
+// Tier M (single nets): both codes, chosen per warp (style 3: the cases while a
+// warp's pairs span at most two rules, the uniform code otherwise) — fib(18)'s
+// narrow rounds keep the cases (2.46 ms; 2.97 with style 1), the wide rounds of
+// A(3,8)'s tier M prefix get the uniform code (profiles/r02ad_style_adaptive.txt).
+int default_style(int tier) { return tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : tier == kTierM ? 3 : 0; }
+
 int tier_style(const inet_ctx* c, int tier) {
   if (c->jit_style >= 0) return c->jit_style;
-  if (tier == kTierC) return 1;
-  if (tier == inetdev::kTierX) return 2;
   if (tier == kTierS) return c->n_nets <= 768 ? 1 : 0;
-  return 0;
+  return default_style(tier);
 }
 
 // CTA size of tier R for a few nets (env INET_B200_RTHREADS overrides; measured).
@@ -1230,7 +1234,7 @@ int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t th
     if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
     std::vector<char> cubin;
     std::string msg;
-    int style = tier == kTierC ? 1 : 0;
+    int style = default_style(tier);
     if (const char* e = std::getenv("INET_B200_JITSTYLE")) style = std::atoi(e);
     bool exact_code = true;
     if (const char* e = std::getenv("INET_B200_EXACTCODE")) exact_code = std::atoi(e) != 0;
@@ -1255,8 +1259,7 @@ int inet_jit_precompile(const uint32_t* blob, size_t n_words, int tier, uint32_t
     if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
     if (tier < kTierS || tier > inetdev::kTierX) return INET_ERR_ARG;
     // as jit_kernel picks it, or flags bits 8-11 = style + 1
-    const int style = (flags >> 8) & 15u ? static_cast<int>(((flags >> 8) & 15u) - 1u)
-                                         : tier == kTierC ? 1 : tier == inetdev::kTierX ? 2 : 0;
+    const int style = (flags >> 8) & 15u ? static_cast<int>(((flags >> 8) & 15u) - 1u) : default_style(tier);
     std::string msg;
     const int rc = inetjit::precompile(
         inetjit::kernel_source(blob, n_words, tier, threads, style, (flags & 1u) != 0, (flags & 2u) != 0,

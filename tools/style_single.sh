@@ -1,7 +1,12 @@
 #!/bin/bash
-# single nets by rule-code style (tier M prefix / tier C)
-for st in "" 1 0; do
+# single nets and batches by rule-code style (unset = the engine's choice)
+for st in unset 3 1; do
   for w in fib18 a38 a310; do
-    echo "style '${st}' $w: $(INET_B200_JITSTYLE=$st timeout 600 python tools/profile_run.py --workload $w --repeat 3 2>&1 | tail -1 | cut -c1-70)"
+    if [ "$st" = unset ]; then
+      echo "style $st $w: $(timeout 600 python tools/profile_run.py --workload $w --repeat 3 2>&1 | tail -1 | cut -c1-70)"
+    else
+      echo "style $st $w: $(INET_B200_JITSTYLE=$st timeout 600 python tools/profile_run.py --workload $w --repeat 3 2>&1 | tail -1 | cut -c1-70)"
+    fi
   done
 done
+echo "== batches, style 3"; INET_B200_JITSTYLE=3 timeout 600 python tools/batch_round_cost.py
