@@ -10,7 +10,13 @@ TESTS = os.path.dirname(os.path.abspath(__file__))
 if TESTS not in sys.path:
     sys.path.insert(0, TESTS)
 
-import paper_1404_0076_b200  # noqa: E402,F401  (makes the reference package `inet` importable)
+try:
+    import paper_1404_0076_b200  # noqa: E402,F401  (makes the reference package `inet` importable)
+except ImportError:  # a fresh checkout: install the reference into baseline/_ref first (build container)
+    import __graft_entry__
+
+    __graft_entry__.ensure_reference()
+    import paper_1404_0076_b200  # noqa: E402,F401
 
 
 def pytest_configure(config):
