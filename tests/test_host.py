@@ -285,3 +285,38 @@ def test_native_flatten_falls_back_for_symbols_outside_the_rules():
     cfg = Configuration((Var(0),), (Equation(Var(0), Agent(Symbol("Q", 0))),))
     prep = engine.prepare([cfg], rules)
     assert "Q" in prep.labels.index
+
+
+# -- right-hand-side-only symbols, private JIT cache ----------
+
+
+def test_symbol_only_on_a_right_hand_side_gets_a_label():
+    """A RuleSet built in code declares only its pattern symbols
+    (core.py:232-239); a symbol that appears only in a rule's right-hand side
+    must still be numbered (it used to raise KeyError in compile_rules)."""
+    from inet.core import Rule, RuleSet
+
+    a, b, c = Symbol("A", 1), Symbol("B", 0), Symbol("C", 0)
+    rs = RuleSet()
+    rs.add(Rule(a, (0,), b, (), (Equation(Var(0), Agent(c)),)))
+    labels = flat.Labels.of(rs)
+    assert "C" in labels.index
+    blob = flat.compile_rules(rs, labels)
+    assert blob[1] == len(labels.symbols)
+
+
+def test_jit_cache_is_private(tmp_path, monkeypatch):
+    """Compiled kernels are cached in a per-user directory created 0700 (not a
+    shared /tmp path another user could plant cubins in)."""
+    from paper_1404_0076_b200 import _native, engine
+
+    monkeypatch.delenv("INET_B200_CACHE", raising=False)
+    monkeypatch.setenv("XDG_CACHE_HOME", str(tmp_path))
+    rules = parse_program("A >< B => ;\nnet : A = B;").rules
+    rules.declare(Symbol("Q", 2))  # a rule set no prebuilt kernel covers
+    prep = engine.prepare([], rules)
+    code, log = _native.jit_compile(prep.blob, 1, 256)
+    assert code == _native.OK, log[:500]
+    d = tmp_path / "inet_b200"
+    assert d.is_dir() and (d.stat().st_mode & 0o777) == 0o700
+    assert any(p.suffix == ".cubin" for p in d.iterdir())
