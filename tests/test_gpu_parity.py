@@ -398,3 +398,17 @@ def test_sharded_batch_gathers_in_input_order():
     for a, b in zip(one.results, two.results):
         assert a.total_interactions == b.total_interactions
         assert print_configuration(a.final) == print_configuration(b.final)
+
+
+def test_symbol_only_on_a_right_hand_side():
+    """A rule set built in code whose right-hand side creates an undeclared
+    symbol: reduced like the reference reduces it."""
+    from inet.core import Rule, RuleSet, Symbol
+
+    a, b, c = Symbol("A", 1), Symbol("B", 0), Symbol("C", 0)
+    rs = RuleSet()
+    rs.add(Rule(a, (0,), b, (), (Equation(Var(0), Agent(c)),)))
+    net = Configuration((Var(5),), (Equation(Agent(a, (Var(5),)), Agent(b)),))
+    res = evaluate(net, rs)
+    assert print_configuration(res.final) == "net C : ;"
+    assert res.total_interactions == 1
