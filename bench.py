@@ -589,6 +589,11 @@ def run_ours(args) -> None:
             if label == "A(3,10)":
                 singles[label]["issue"] = ncu_issue("a310")
             singles[label]["e2e_path"] = "evaluate_text(config, rules): flatten + H2D + reduce + D2H + finalize + print"
+            # the reference's own call: evaluate() returning reference term objects (EvalResult.final)
+            t0 = time.perf_counter()
+            res = engine.evaluate(p.build_input(*pparams), p.rules, EngineConfig(collect_stats=False))
+            singles[label]["evaluate_ms"] = 1000.0 * (time.perf_counter() - t0)
+            assert res.total_interactions == golden
             c2.close()
         line["single_nets"] = singles
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
