@@ -158,7 +158,9 @@ int inet_jit_compile(const uint32_t* blob, size_t n_words, int tier, uint32_t th
  * into the package's kernels/ directory next to the library, where every
  * later process finds it without running NVRTC (the shipped programs are
  * precompiled by the package build). flags: bit 0 reference-loop code
- * (deferred equations), bit 1 per-rule counters. */
+ * (deferred equations), bit 1 per-rule counters, bit 2 reference-ordered
+ * var = var keys (stamps), bit 3 without per-round rows (collect_stats off),
+ * bits 8-11 code style + 1 (0: the tier's default). */
 int inet_jit_precompile(const uint32_t* blob, size_t n_words, int tier, uint32_t threads, uint32_t flags, char* log,
                         size_t log_len);
 

@@ -411,12 +411,12 @@ TIER_S, TIER_M, TIER_G, TIER_C, TIER_X, TIER_R = 0, 1, 2, 3, 4, 5
 
 
 def jit_precompile(blob: np.ndarray, tier: int, threads: int, exact_code: bool, count_rules: bool,
-                   stamps: bool = False, style: int = -1) -> tuple[int, str]:
+                   stamps: bool = False, style: int = -1, rows: bool = True) -> tuple[int, str]:
     """Compile one kernel variant into the package's kernels/ directory (build time)."""
     lib = load_library()
     blob = np.ascontiguousarray(blob, dtype=np.uint32)
     log = C.create_string_buffer(1 << 16)
-    flags = (1 if exact_code else 0) | (2 if count_rules else 0) | (4 if stamps else 0) | ((style + 1) << 8)
+    flags = (1 if exact_code else 0) | (2 if count_rules else 0) | (4 if stamps else 0) | (0 if rows else 8) | ((style + 1) << 8)
     code = lib.inet_jit_precompile(_ptr(blob), blob.size, tier, threads, flags, log, len(log))
     return code, log.value.decode(errors="replace")
 

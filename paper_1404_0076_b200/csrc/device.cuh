@@ -258,6 +258,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Per-round rows (EvalResult.loops): the rule-set kernels are compiled with or
+// without them (jit.cpp kernel_source); the prebuilt kernels decide at run time.
+#ifndef INET_ROWS
+#define INET_ROWS 1
+#endif
+
 #ifdef INET_TIMING
 // Development build only: per-phase clock64 totals (tools/phase_timing.py).
 #define INET_TMARK(c, k)                  \
@@ -1349,7 +1355,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   // thread keeps its own running totals, summed once after the loop. (Tier
   // M's hand-over threshold counts queued pairs instead: the pairs queued in
   // round r are exactly the interactions of round r + 1.)
-  const bool per_round = d.stats != nullptr;
+  const bool per_round = INET_ROWS && d.stats != nullptr;
   unsigned long long tot_q = 0;
   c.ints = c.comms = 0;
   c.parked = 0;
@@ -1372,7 +1378,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       c.parked = 0;
     }
     if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(&ctl->ctr3[set_next])[threadIdx.x] = 0;
-    c.dout = sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
+    c.dout = INET_EXACT_CODE && sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
     c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + (r & 1u) * qstride)
                        : static_cast<void*>(static_cast<uint2*>(q0) + (r & 1u) * qstride);
     if (INET_EXACT_CODE && nd) {
@@ -1478,7 +1484,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     }
     set = set_next;
     set_next = set_next == 2 ? 0u : set_next + 1;
-    if (threadIdx.x == 0 && d.stats) {
+    if (per_round && threadIdx.x == 0) {
 #ifdef INET_NO_TIMER
       const unsigned long long now = 0;
 #else
@@ -1510,7 +1516,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     } else if (q == 0 && nd == 0) {
       // the trailing no-op loop the reference records (engine.py:222-223)
       stop = true;
-      if (threadIdx.x == 0 && d.stats && r < d.cap_rounds)
+      if (per_round && threadIdx.x == 0 && r < d.cap_rounds)
         d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
     } else if (kTier == kTierM && sh.promote_ints && (tot_q += q) >= sh.promote_ints) {
       stop = true;  // a large net: the host hands it over to a cluster
@@ -1772,7 +1778,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
   const bool writer = rank == 0 && threadIdx.x == 0;
   // per-round totals only for the per-round rows; otherwise per-thread
   // running totals, summed once after the loop
-  const bool per_round = d.stats != nullptr;
+  const bool per_round = INET_ROWS && d.stats != nullptr;
   c.ints = c.comms = 0;
   c.parked = 0;
   if (!fits) {
@@ -1797,7 +1803,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
       c.parked = 0;
     }
     c.inq = lqueue + (r & 1u) * 16 * cap_q;
-    c.dout = sh.exact ? d.deferred + ((r & 1u) * G + rank) * c.cap_def : nullptr;
+    c.dout = INET_EXACT_CODE && sh.exact ? d.deferred + ((r & 1u) * G + rank) * c.cap_def : nullptr;
     c.outc = outc3 + (r % 3) * 32;
     c.mbox_a = mbox + (r & 1u) * 2 * 16 * kMbox;
     c.mbox_v = c.mbox_a + 16 * kMbox;
@@ -1968,7 +1974,7 @@ __device__ void run_net_cluster(const NetDesc& d, const Shape& sh, const uint16_
         tot_i += ri;
         tot_c += rc;
         parked_tot += rp;
-        if (d.stats) {
+        if (per_round) {
 #ifdef INET_NO_TIMER
           const unsigned long long now = 0;
 #else
@@ -2205,7 +2211,7 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
   uint2* const Q = d.queue;
   // per-round totals only for the per-round rows (every block's atomics on
   // three global counters each round otherwise)
-  const bool per_round = d.stats != nullptr;
+  const bool per_round = INET_ROWS && d.stats != nullptr;
   c.ints = c.comms = 0;
   c.parked = 0;
   for (uint32_t r = 1; !stop; ++r) {
@@ -2273,7 +2279,7 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
     parked_tot += k.parked;
     tot_i += k.ints;
     tot_c += k.comms;
-    if (lead && d.stats) {
+    if (per_round && lead) {
       const unsigned long long now = globaltimer();
       if (r - 1 < d.cap_rounds)
         d.stats[r - 1] = make_uint4(k.ints, k.comms, q + static_cast<uint32_t>(parked_tot),
@@ -2292,7 +2298,7 @@ __device__ void run_net_grid(const NetDesc& d, const Shape& sh, const uint16_t* 
       stop_err = INET_ERR_LOOP_CAP;
     } else if (q == 0) {
       stop = true;
-      if (lead && d.stats && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
+      if (per_round && lead && r < d.cap_rounds) d.stats[r] = make_uint4(0, 0, static_cast<uint32_t>(parked_tot), 0);
     } else if (q > c.cap_queue) {
       stop = true;
       stop_err = INET_ERR_ARENA;

@@ -565,13 +565,16 @@ const void* jit_kernel(inet_ctx* c, int tier, uint32_t threads) {
   // code style per tier: straight-line cases where the rewrite is issue-bound
   // (S, M, G); a uniform memory phase where remote latency dominates (C)
   const int style = tier_style(c, tier);
+  // per-round rows compiled in only when this layout records them (cap_rounds)
+  const bool rows = c->cap_rounds != 0;
   const auto key = std::make_tuple(tier, threads,
-                                   style + (c->exact_code ? 16 : 0) + (c->count_rules ? 32 : 0) + (c->var_order ? 64 : 0));
+                                   style + (c->exact_code ? 16 : 0) + (c->count_rules ? 32 : 0) + (c->var_order ? 64 : 0) +
+                                       (rows ? 128 : 0));
   auto it = c->jit_kernels.find(key);
   if (it != c->jit_kernels.end()) return reinterpret_cast<const void*>(it->second.second);
   const std::string src =
       inetjit::kernel_source(c->blob.data(), c->blob.size(), tier, threads, style, c->exact_code, c->count_rules,
-                             c->var_order);
+                             c->var_order, rows);
   std::vector<char> cubin;
   if (inetjit::compile_cubin(src, cubin, c->jit_log) != 0) {
     std::fprintf(stderr, "inet_b200: rule-set JIT unavailable, using the prebuilt kernels: %s\n", c->jit_log.c_str());
@@ -903,8 +906,8 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     c->tier = tier;
     c->shape = sh;
     if (std::getenv("INET_B200_DEBUG"))
-      std::fprintf(stderr, "inet_b200: attempt tier %d caps %u/%u/%u: %.3f ms, net 0 status 0x%x\n", tier, ca, cv, cq, ms,
-                   c->ctl[0].err);
+      std::fprintf(stderr, "inet_b200: attempt tier %d caps %u/%u/%u: %.3f ms, net 0 status 0x%x (%u, %u)\n", tier, ca, cv,
+                   cq, ms, c->ctl[0].err, c->ctl[0].err_a, c->ctl[0].err_b);
     return INET_OK;
   };
   if (!user_caps && c->n_nets > 1 && c->max_in_agents <= 512 && c->max_in_vars <= 512) {
@@ -939,9 +942,23 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   // past 2^19 interactions tier M hands it over — arena, slot table, pending
   // equations, rounds and totals — and a 16-CTA cluster (tier C) resumes it
   // from there, which wins once rounds are wide. 1 forces one CTA per net.
+  if (const char* e = std::getenv("INET_B200_SINGLE_S"); e && !done && c->n_nets == 1 && !user_caps) {
+    // development: a single net on tier S with these capacities (agents,vars,queue,ring)
+    unsigned a = 0, v = 0, q = 0, rg = 0;
+    if (std::sscanf(e, "%u,%u,%u,%u", &a, &v, &q, &rg) == 4) {
+      Shape sh = base_shape(c, max_loops);
+      sh.res_agents = a;
+      sh.res_vars = v;
+      sh.res_queue = q;
+      sh.ring_a = sh.ring_v = rg;
+      const int st = attempt_tier(kTierS, sh, a, v, 1);
+      if (st == INET_OK && !any_oom()) done = true;
+      else if (st != INET_OK && st != INET_ERR_UNSUPPORTED) return st;
+    }
+  }
   uint32_t want_g = cfg ? cfg->ctas_per_net : 0;
   if (c->var_order) want_g = 1;  // no cluster or whole-GPU tier: one CTA, tier M then G
-  if (want_g == 0 && c->n_nets == 1 && !user_caps) {
+  if (!done && want_g == 0 && c->n_nets == 1 && !user_caps) {
     want_g = 16;
     if (c->max_in_agents < 32768 && c->max_in_vars < 16384) {
       Shape sh = base_shape(c, max_loops);
@@ -1258,12 +1275,12 @@ int inet_jit_precompile(const uint32_t* blob, size_t n_words, int tier, uint32_t
     if (!blob || n_words < 4) return INET_ERR_ARG;
     if (int st = inethost::validate_rule_blob(blob, n_words)) return st;
     if (tier < kTierS || tier > inetdev::kTierX) return INET_ERR_ARG;
-    // as jit_kernel picks it, or flags bits 8-11 = style + 1
+    // as jit_kernel picks it, or flags bits 8-11 = style + 1; bit 3: without per-round rows
     const int style = (flags >> 8) & 15u ? static_cast<int>(((flags >> 8) & 15u) - 1u) : default_style(tier);
     std::string msg;
     const int rc = inetjit::precompile(
         inetjit::kernel_source(blob, n_words, tier, threads, style, (flags & 1u) != 0, (flags & 2u) != 0,
-                               (flags & 4u) != 0),
+                               (flags & 4u) != 0, (flags & 8u) == 0),
         msg);
     if (log && log_len) {
       std::strncpy(log, msg.c_str(), log_len - 1);

@@ -51,21 +51,23 @@ def precompile_shipped(workers: int = 8) -> list:
     for name, blob in shipped_blobs().items():
         for tier, threads, style in VARIANTS:
             for exact in (False, True):
-                jobs.append((name, blob, tier, threads, exact, False, False, style))
+                for rows in (False, True):
+                    jobs.append((name, blob, tier, threads, exact, False, False, style, rows))
         if name in ("fibonacci", "addition", "arith"):
             for tier, threads, style in STAMP_VARIANTS:
                 for exact in (False, True):
-                    jobs.append((name, blob, tier, threads, exact, False, True, style))
+                    for rows in (False, True):
+                        jobs.append((name, blob, tier, threads, exact, False, True, style, rows))
         # accounting runs of bench.py (per-rule histogram)
         if name in ("ackermann", "lsystem", "fibonacci"):
             for tier, threads, style in ((_native.TIER_S, 128, 0), (_native.TIER_M, 256, -1),
                                          (_native.TIER_C, 256, -1), (_native.TIER_X, 256, -1)):
-                jobs.append((name, blob, tier, threads, False, True, False, style))
+                jobs.append((name, blob, tier, threads, False, True, False, style, False))
     failed = []
 
     def one(job):
-        name, blob, tier, threads, exact, count, stamps, style = job
-        code, log = _native.jit_precompile(blob, tier, threads, exact, count, stamps, style)
+        name, blob, tier, threads, exact, count, stamps, style, rows = job
+        code, log = _native.jit_precompile(blob, tier, threads, exact, count, stamps, style, rows)
         if code != 0:
             failed.append((name, tier, threads, exact, count, log[-400:]))
 
