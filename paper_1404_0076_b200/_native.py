@@ -95,6 +95,25 @@ _u32p = C.POINTER(C.c_uint32)
 _u64p = C.POINTER(C.c_uint64)
 
 
+def _choose_nvrtc() -> None:
+    """Point the rule-set compiler at the NVRTC that ships with torch's CUDA
+    runtime (the `nvidia-cuda-nvrtc` wheel) when it is installed, so the
+    compiler does not depend on which libnvrtc.so.12 a process loaded first.
+    Its code measured faster than the system toolkit's on the shipped
+    programs. INET_B200_NVRTC set by the user wins."""
+    if os.environ.get("INET_B200_NVRTC"):
+        return
+    try:
+        import nvidia.cuda_nvrtc as nv
+    except ImportError:
+        return
+    for base in getattr(nv, "__path__", []):
+        cand = os.path.join(base, "lib", "libnvrtc.so.12")
+        if os.path.exists(cand):
+            os.environ["INET_B200_NVRTC"] = cand
+            return
+
+
 def load_library(path: str = LIB_PATH) -> C.CDLL:
     """Load the shared object and declare every exported signature."""
     global _lib
@@ -103,6 +122,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             return _lib
         if not os.path.exists(path):
             raise DeviceError(-1, f"native library not built: {path} (run `python __graft_entry__.py`)")
+        _choose_nvrtc()
         lib = C.CDLL(path)
         sig = {
             "inet_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
