@@ -665,14 +665,19 @@ __device__ __forceinline__ void warp_push(Round<kTier>& c, bool pu, uint32_t l, 
 constexpr uint32_t kOrderUndecided = INET_ERR_ORDER;
 
 template <int kTier>
-__device__ __forceinline__ void stamp_fresh(const Round<kTier>& c, uint32_t x, uint32_t j) {
+__device__ __forceinline__ void stamp_store(const Round<kTier>& c, uint32_t x, uint32_t j) {
 #if INET_STAMPS
-  if (c.stamps) {
+  if (c.stamps)
     c.stamps[x & ~vtag<kTier>()] =
         (static_cast<unsigned long long>(c.round) << 40) | (static_cast<unsigned long long>(c.cid) << 8) | j;
-    // ordered before the exchange that may hand x to another thread this round
-    __threadfence_block();
-  }
+#endif
+}
+// One fence after a rewrite's stamps: ordered before the exchange that may hand
+// a fresh variable to another thread this round.
+template <int kTier>
+__device__ __forceinline__ void stamp_publish(const Round<kTier>& c) {
+#if INET_STAMPS
+  if (c.stamps) __threadfence_block();
 #endif
 }
 
@@ -768,8 +773,9 @@ __device__ __forceinline__ bool jit_alloc_vars(Round<kTier>& c, uint32_t (&f)[N]
 #pragma unroll
   for (uint32_t j = 0; j < N; ++j) {
     f[j] = vtag<kTier>() | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
-    stamp_fresh(c, f[j], j);
+    stamp_store(c, f[j], j);
   }
+  stamp_publish(c);
   return true;
 }
 
@@ -792,8 +798,9 @@ __device__ __forceinline__ bool jit_alloc_vars_n(Round<kTier>& c, uint32_t n, ui
   for (uint32_t j = 0; j < N; ++j)
     if (j < n) {
       f[j] = vtag<kTier>() | (j < k.got ? static_cast<uint32_t>(c.vring[(k.pos + j) & c.vmask]) : bump_var(c, k.bump + (j - k.got)));
-      stamp_fresh(c, f[j], j);
+      stamp_store(c, f[j], j);
     }
+  stamp_publish(c);
   return true;
 }
 
@@ -910,10 +917,12 @@ __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uin
 #pragma unroll
   for (uint32_t j = 0; j < MX; ++j) g[j] = j < ga ? ra[j] : bump_agent(c, ba + (j - ga));
 #if INET_STAMPS
-  if (c.stamps)
+  if (c.stamps && nf) {
 #pragma unroll
     for (uint32_t j = 0; j < MF; ++j)
-      if (j < nf) stamp_fresh(c, f[j], j);
+      if (j < nf) stamp_store(c, f[j], j);
+    stamp_publish(c);
+  }
 #endif
   return true;
 }
@@ -982,8 +991,10 @@ __device__ __forceinline__ void interact(Round<kTier>& c, uint32_t l, uint32_t r
     return q < na.got ? static_cast<uint32_t>(c.aring[(na.pos + q) & c.amask]) : bump_agent(c, na.bump + (q - na.got));
   };
 #if INET_STAMPS
-  if (c.stamps)
-    for (uint32_t j = 0; j < nf; ++j) stamp_fresh(c, fresh(j), j);
+  if (c.stamps && nf) {
+    for (uint32_t j = 0; j < nf; ++j) stamp_store(c, fresh(j), j);
+    stamp_publish(c);
+  }
 #endif
   uint32_t env_l[Traits<kTier>::kEnvLocal ? kEnvSize : 1];
   if constexpr (Traits<kTier>::kEnvLocal) {
