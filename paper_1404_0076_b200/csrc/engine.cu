@@ -225,6 +225,13 @@ struct inet_ctx {
   std::vector<NetCtl> ctl;
   std::vector<inet_net_stats> stats;
   PinnedU32 h_agents;                 // per-net slab prefixes [n_nets * agent_pitch * 4]
+  // Tier S batches write their results (the device-finalized normal forms, or
+  // the arena for the host to finalize) straight into page-locked host memory
+  // the device addresses directly, so no copy follows the kernel: the nets
+  // of a wave write theirs while the next wave computes.
+  PinnedU32 h_zc;                     // [n_nets * cap_agents * 4]
+  bool zc_next = false;               // the next layout puts tier S results in h_zc
+  bool zc_used = false;               // the last run's results are in h_zc (pitch cap_agents)
   PinnedU32 h_resid;                  // [n_nets * resid_pitch * 2]
   uint32_t agent_pitch = 0, resid_pitch = 0;
   std::vector<uint32_t> h_rounds;     // [n_nets * rows_pitch * 4]
@@ -248,6 +255,8 @@ struct inet_ctx {
 };
 
 inline uint32_t hist_stride(const inet_ctx* c) { return std::max(c->n_rules, 128u); }
+// the last run's agent records on the host (pitch agent_pitch records per net)
+inline const uint32_t* host_agents(const inet_ctx& c) { return c.zc_used ? c.h_zc.data() : c.h_agents.data(); }
 
 #define CUDA_TRY(expr)                                                                         \
   do {                                                                                         \
@@ -438,6 +447,16 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
   c->cap_queue = cap_queue;
   c->cap_rounds = cap_rounds;
   const size_t N = n;
+  uint4* zc = nullptr;  // tier S results in mapped host memory (see h_zc)
+  if (c->zc_next) {
+    c->h_zc.resize(N * cap_agents * 4);
+    void* dp = nullptr;
+    if (c->h_zc.pinned && cudaHostGetDevicePointer(&dp, c->h_zc.data(), 0) == cudaSuccess)
+      zc = static_cast<uint4*>(dp);
+    else
+      cudaGetLastError();
+  }
+  c->zc_used = zc != nullptr;
   if (c->d_agents.ensure(N * cap_agents * 16) || c->d_vslot.ensure(N * cap_vars * 4) ||
       c->d_queue.ensure(N * 2 * cap_queue * 8) || c->d_resid.ensure(N * cap_vars * 8) ||
       c->d_ctl.ensure(N * sizeof(NetCtl)) || c->d_desc.ensure(N * sizeof(NetDesc)) ||
@@ -456,7 +475,7 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
   for (uint32_t i = 0; i < n; ++i) {
     NetDesc& d = desc[i];
     std::memset(&d, 0, sizeof(d));
-    d.agents = static_cast<uint4*>(c->d_agents.p) + size_t(i) * cap_agents;
+    d.agents = (zc ? zc : static_cast<uint4*>(c->d_agents.p)) + size_t(i) * cap_agents;
     d.vslot = static_cast<uint32_t*>(c->d_vslot.p) + size_t(i) * cap_vars;
     d.queue = static_cast<uint2*>(c->d_queue.p) + size_t(i) * 2 * cap_queue;
     d.stats = cap_rounds ? static_cast<uint4*>(c->d_stats.p) + size_t(i) * cap_rounds : nullptr;
@@ -927,7 +946,9 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
           sh.ring_a = sh.ring_v = rg;
         }
       }
+      c->zc_next = c->dev_final;
       int st = attempt_tier(kTierS, sh, sh.res_agents, sh.res_vars, 1);
+      c->zc_next = false;
       if (st == INET_OK && !any_oom()) {
         done = true;
         break;
@@ -1114,11 +1135,11 @@ int finish_run(inet_ctx* c, bool fetch) {
       max_res = std::max(max_res, dev ? c->ctl[i].pad[2] : s.n_residual);
     }
     // strided copies of each slab's used prefix
-    c->agent_pitch = std::max(max_hw, 1u);
+    c->agent_pitch = c->zc_used ? c->cap_agents : std::max(max_hw, 1u);
     c->resid_pitch = std::max(max_res, 1u);
-    c->h_agents.resize(size_t(c->n_nets) * c->agent_pitch * 4);
+    if (!c->zc_used) c->h_agents.resize(size_t(c->n_nets) * c->agent_pitch * 4);
     c->h_resid.resize(size_t(c->n_nets) * c->resid_pitch * 2);
-    if (max_hw)
+    if (max_hw && !c->zc_used)
       CUDA_TRY(cudaMemcpy2DAsync(c->h_agents.data(), size_t(c->agent_pitch) * 16, c->d_agents.p,
                                  size_t(c->cap_agents) * 16, size_t(max_hw) * 16, c->n_nets, cudaMemcpyDeviceToHost,
                                  c->stream));
@@ -1198,9 +1219,11 @@ int inet_batch_rerun(inet_ctx* c, const inet_cfg* cfg, float* device_ms) {
     }
     c->grid_tier = c->tier == inetdev::kTierX;
     c->ordered_tier = c->tier == inetdev::kTierR;
+    c->zc_next = c->tier == kTierS && c->dev_final && c->n_nets > 1;
     int st = layout(c, c->cap_agents, c->cap_vars, c->cap_queue, cap_rounds);
     c->grid_tier = false;
     c->ordered_tier = false;
+    c->zc_next = false;
     if (st) return st;
     Shape sh = c->shape;
     sh.max_rounds = k.max_loops;
@@ -1547,7 +1570,7 @@ int finalize_batch(inet_ctx& c, uint32_t net, uint32_t n_threads) {
     if (const uint32_t rows = i < c.dev_rows.size() ? c.dev_rows[i] : 0u) {
       // finalized on the device: copy out the compacted normal form
       NormalForm& nf = c.results[i];
-      const uint32_t* ag = c.h_agents.data() + size_t(i) * c.agent_pitch * 4;
+      const uint32_t* ag = host_agents(c) + size_t(i) * c.agent_pitch * 4;
       const uint32_t* rs = c.h_resid.data() + size_t(i) * c.resid_pitch * 2;
       const uint32_t ni = static_cast<uint32_t>(c.iface_off[i + 1] - c.iface_off[i]);
       nf.agents.clear();
@@ -1560,7 +1583,7 @@ int finalize_batch(inet_ctx& c, uint32_t net, uint32_t n_threads) {
       return INET_OK;
     }
     NetView v;
-    v.agents = c.h_agents.data() + size_t(i) * c.agent_pitch * 4;
+    v.agents = host_agents(c) + size_t(i) * c.agent_pitch * 4;
     v.n_agents = s.agent_hw;
     v.residual = c.h_resid.data() + size_t(i) * c.resid_pitch * 2;
     v.n_residual = s.n_residual;
