@@ -528,11 +528,29 @@ __device__ __forceinline__ void st_slot(const Round<kTier>& c, uint32_t x, uint3
   else c.vslot[x] = v;
 }
 
+// Ring claims of a round. Tiers S and M count both in one word (agents in the
+// low half, variables in the high half: a round takes fewer than 2^16 of
+// either), so a rewrite that needs both claims them with one shared-memory
+// atomic — same-address atomics serialise per lane, and the counters are the
+// batch kernel's busiest shared-memory traffic.
+template <int kTier>
+constexpr bool kTake2 = kTier == kTierS || kTier == kTierM;
+template <int kTier>
+__device__ __forceinline__ uint32_t take_vars(Round<kTier>& c, uint32_t n) {
+  if constexpr (kTake2<kTier>) return atomicAdd(&c.cur->atake, n << 16) >> 16;
+  else return atomicAdd(&c.cur->vtake, n);
+}
+template <int kTier>
+__device__ __forceinline__ uint32_t take_agents(Round<kTier>& c, uint32_t n) {
+  if constexpr (kTake2<kTier>) return atomicAdd(&c.cur->atake, n) & 0xFFFFu;
+  else return atomicAdd(&c.cur->atake, n);
+}
+
 template <int kTier>
 __device__ __forceinline__ bool alloc_vars(Round<kTier>& c, uint32_t nf, Claim& k) {
   k.pos = k.got = k.bump = 0;
   if (nf == 0) return true;
-  const uint32_t t = atomicAdd(&c.cur->vtake, nf);
+  const uint32_t t = take_vars(c, nf);
   const uint32_t avail = c.hi_v - c.lo_v;
   k.pos = c.lo_v + t;
   if (t < avail) k.got = min(avail - t, nf);
@@ -551,7 +569,7 @@ template <int kTier>
 __device__ __forceinline__ bool alloc_agents(Round<kTier>& c, uint32_t n, Claim& k) {
   k.pos = k.got = k.bump = 0;
   if (n == 0) return true;
-  const uint32_t t = atomicAdd(&c.cur->atake, n);
+  const uint32_t t = take_agents(c, n);
   const uint32_t avail = c.hi_a - c.lo_a;
   k.pos = c.lo_a + t;
   if (t < avail) k.got = min(avail - t, n);
@@ -830,8 +848,14 @@ __device__ __forceinline__ bool jit_warp_alloc(Round<kTier>& c, uint32_t nf, uin
   const uint32_t av_v = c.hi_v - c.lo_v, av_a = c.hi_a - c.lo_a;
   uint32_t tv = 0, ta = 0, bv = 0, ba = 0, ok = 1;
   if (lane == 0) {
-    if (tot_f) tv = atomicAdd(&c.cur->vtake, tot_f);
-    if (tot_x) ta = atomicAdd(&c.cur->atake, tot_x);
+    if constexpr (kTake2<kTier>) {
+      const uint32_t w = atomicAdd(&c.cur->atake, (tot_f << 16) | tot_x);
+      tv = w >> 16;
+      ta = w & 0xFFFFu;
+    } else {
+      if (tot_f) tv = atomicAdd(&c.cur->vtake, tot_f);
+      if (tot_x) ta = atomicAdd(&c.cur->atake, tot_x);
+    }
     const uint32_t ov = tv + tot_f > av_v ? tv + tot_f - max(tv, av_v) : 0u;
     const uint32_t oa = ta + tot_x > av_a ? ta + tot_x - max(ta, av_a) : 0u;
     if (ov) {
@@ -885,8 +909,15 @@ template <uint32_t MF, uint32_t MX, int kTier>
 __device__ __forceinline__ bool jit_alloc_both(Round<kTier>& c, uint32_t nf, uint32_t nx, uint32_t (&f)[MF],
                                                uint32_t (&g)[MX]) {
   if ((nf | nx) == 0) return true;
-  const uint32_t tv = nf ? atomicAdd(&c.cur->vtake, nf) : 0u;
-  const uint32_t ta = nx ? atomicAdd(&c.cur->atake, nx) : 0u;
+  uint32_t tv = 0, ta = 0;
+  if constexpr (kTake2<kTier>) {
+    const uint32_t w = atomicAdd(&c.cur->atake, (nf << 16) | nx);
+    tv = w >> 16;
+    ta = w & 0xFFFFu;
+  } else {
+    tv = nf ? atomicAdd(&c.cur->vtake, nf) : 0u;
+    ta = nx ? atomicAdd(&c.cur->atake, nx) : 0u;
+  }
   const uint32_t av_v = c.hi_v - c.lo_v, av_a = c.hi_a - c.lo_a;
 
   const uint32_t gv = tv < av_v ? min(av_v - tv, nf) : 0u, ga = ta < av_a ? min(av_a - ta, nx) : 0u;
@@ -1484,9 +1515,11 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     // frees of round r were kept while they fit the ring (against its old window)
     const uint32_t wa = min(k.afree, sh.ring_a - (hi_a - lo_a));
     const uint32_t wv = min(k.vfree, sh.ring_v - (hi_v - lo_v));
-    lo_a += min(k.atake, hi_a - lo_a);
+    const uint32_t atake = kTake2<kTier> ? (k.atake & 0xFFFFu) : k.atake;
+    const uint32_t vtake = kTake2<kTier> ? (k.atake >> 16) : k.vtake;
+    lo_a += min(atake, hi_a - lo_a);
     hi_a += wa;
-    lo_v += min(k.vtake, hi_v - lo_v);
+    lo_v += min(vtake, hi_v - lo_v);
     hi_v += wv;
     if (per_round) {
       parked_tot += k.parked;
