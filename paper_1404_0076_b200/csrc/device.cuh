@@ -607,6 +607,19 @@ __device__ __forceinline__ void free_agent(Round<kTier>& c, uint32_t a) {
   if (pos - c.lo_a <= c.amask) c.aring[pos & c.amask] = a;  // else dropped
 }
 
+// Tiers S and M count queued pairs in the low half of vfree (freed variables
+// in the high half; a round queues and frees fewer than 2^16 of each), so a
+// merge that frees its variable and queues the active pair it formed takes
+// one shared-memory atomic. qcount then only carries the failure bit.
+template <int kTier>
+constexpr bool kPush2 = kTier == kTierS || kTier == kTierM;
+
+template <int kTier>
+__device__ __forceinline__ void ring_var(Round<kTier>& c, uint32_t x, uint32_t f) {
+  const uint32_t pos = c.hi_v + f;
+  if (pos - c.lo_v <= c.vmask) c.vring[pos & c.vmask] = x;
+}
+
 template <int kTier>
 __device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
   if constexpr (kTier == kTierC) {
@@ -614,9 +627,11 @@ __device__ __forceinline__ void free_var(Round<kTier>& c, uint32_t x) {
                c.mbox_v, c.vslot);
     return;
   }
-  const uint32_t f = kTier == kTierX ? agg_add(&c.cur->vfree) : atomicAdd(&c.cur->vfree, 1u);
-  const uint32_t pos = c.hi_v + f;
-  if (pos - c.lo_v <= c.vmask) c.vring[pos & c.vmask] = x;
+  if constexpr (kPush2<kTier>) {
+    ring_var(c, x, atomicAdd(&c.cur->vfree, 1u << 16) >> 16);
+    return;
+  }
+  ring_var(c, x, kTier == kTierX ? agg_add(&c.cur->vfree) : atomicAdd(&c.cur->vfree, 1u));
 }
 
 __device__ __forceinline__ void dsmem_st2(const void* p, uint32_t rank, uint2 v) {
@@ -627,7 +642,23 @@ __device__ __forceinline__ void dsmem_st2(const void* p, uint32_t rank, uint2 v)
 // cluster (the p-th to CTA (p + rank) mod G, slot p / G) straight into the
 // consumer's shared memory, so next round every CTA reads its pairs locally.
 template <int kTier>
+__device__ __forceinline__ void queue_at(Round<kTier>& c, uint32_t p, uint32_t l, uint32_t r) {  // tiers S/M/G/X
+  if (p >= c.cap_queue) {
+    fail(c, INET_ERR_ARENA, 2);
+    return;
+  }
+  if constexpr (Traits<kTier>::kPacked)
+    static_cast<uint32_t*>(c.out)[p] = (l << 16) | r;  // both < 65536 in tiers S/M
+  else
+    static_cast<uint2*>(c.out)[p] = make_uint2(l, r);
+}
+
+template <int kTier>
 __device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_t r) {
+  if constexpr (kPush2<kTier>) {
+    queue_at(c, atomicAdd(&c.cur->vfree, 1u) & 0xFFFFu, l, r);
+    return;
+  }
   const uint32_t p = kTier == kTierX ? agg_add(&c.cur->qcount) : atomicAdd(&c.cur->qcount, 1u);
   if constexpr (kTier == kTierC) {
     const uint32_t s = (p & ~kErrBit) >> c.gshift;
@@ -638,14 +669,7 @@ __device__ __forceinline__ void push_active(Round<kTier>& c, uint32_t l, uint32_
     dsmem_st2(&c.inq[c.rank * c.qj + s], (p + c.rank) & (c.stride - 1), make_uint2(l, r));
     return;
   }
-  if (p >= c.cap_queue) {
-    fail(c, INET_ERR_ARENA, 2);
-    return;
-  }
-  if constexpr (Traits<kTier>::kPacked)
-    static_cast<uint32_t*>(c.out)[p] = (l << 16) | r;  // both < 65536 in tiers S/M
-  else
-    static_cast<uint2*>(c.out)[p] = make_uint2(l, r);
+  queue_at(c, p, l, r);
 }
 
 // Warp-collective push: every lane calls it, lanes with `pu` push (l, r).
@@ -659,7 +683,9 @@ __device__ __forceinline__ void warp_push(Round<kTier>& c, bool pu, uint32_t l, 
   if (!m) return;
   const uint32_t lane = threadIdx.x & 31u, leader = __ffs(m) - 1;
   uint32_t base = 0;
-  if (lane == leader) base = atomicAdd(&c.cur->qcount, static_cast<uint32_t>(__popc(m)));
+  if (lane == leader)
+    base = kPush2<kTier> ? atomicAdd(&c.cur->vfree, static_cast<uint32_t>(__popc(m))) & 0xFFFFu
+                         : atomicAdd(&c.cur->qcount, static_cast<uint32_t>(__popc(m)));
   base = __shfl_sync(0xFFFFFFFFu, base, leader);
   if (!pu) return;
   const uint32_t p = base + __popc(m & ((1u << lane) - 1u));
@@ -743,11 +769,21 @@ __device__ __forceinline__ void settle(Round<kTier>& c, uint32_t x, uint32_t old
     if constexpr (kTier != kTierC) st_slot(c, x, kNone);
     c.comms += 1;
     c.parked -= 1;
-    free_var(c, x);
     const uint32_t l = old, r = val;
-    if (((l | r) & kVar) == 0) {
-      push_active(c, l, r);
-      return;
+    if constexpr (kPush2<kTier>) {
+      if (((l | r) & kVar) == 0) {  // free x and queue (l, r): one atomic
+        const uint32_t w = atomicAdd(&c.cur->vfree, (1u << 16) | 1u);
+        ring_var(c, x, w >> 16);
+        queue_at(c, w & 0xFFFFu, l, r);
+        return;
+      }
+      ring_var(c, x, atomicAdd(&c.cur->vfree, 1u << 16) >> 16);
+    } else {
+      free_var(c, x);
+      if (((l | r) & kVar) == 0) {
+        push_active(c, l, r);
+        return;
+      }
     }
 #if INET_EXACT_CODE
     if (c.dout) {
@@ -1505,7 +1541,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     // ---- close round r (every thread, same values)
     const RoundCtr k = *cur;
     bool round_failed = (k.qcount & kErrBit) != 0;
-    const uint32_t q = k.qcount & ~kErrBit;
+    const uint32_t q = kPush2<kTier> ? (k.vfree & 0xFFFFu) : (k.qcount & ~kErrBit);
 #if INET_EXACT_CODE
     if (k.dcount > d.cap_def) {
       round_failed = true;
@@ -1514,7 +1550,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
 #endif
     // frees of round r were kept while they fit the ring (against its old window)
     const uint32_t wa = min(k.afree, sh.ring_a - (hi_a - lo_a));
-    const uint32_t wv = min(k.vfree, sh.ring_v - (hi_v - lo_v));
+    const uint32_t wv = min(kPush2<kTier> ? (k.vfree >> 16) : k.vfree, sh.ring_v - (hi_v - lo_v));
     const uint32_t atake = kTake2<kTier> ? (k.atake & 0xFFFFu) : k.atake;
     const uint32_t vtake = kTake2<kTier> ? (k.atake >> 16) : k.vtake;
     lo_a += min(atake, hi_a - lo_a);
