@@ -1440,9 +1440,15 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   uint32_t lo_a = 0, hi_a = 0, lo_v = 0, hi_v = 0, n = d.n_in_eqs, nd = 0, rounds = 1;
   int32_t parked_tot = 0;
   unsigned long long tot_i = 0, tot_c = 0, t_prev = globaltimer();
-  uint32_t set = 1, set_next = 2;  // r % 3 and (r + 1) % 3, rotated
+  // counter sets r % 3 (this round), (r + 1) % 3 (cleared now), (r + 2) % 3
+  // (read by the previous round's close), rotated as pointers
+  RoundCtr *cur = &ctl->ctr3[1], *nxt = &ctl->ctr3[2], *old = &ctl->ctr3[0];
+  // queue buffers: this round's input and output, swapped every round
+  char* q_in = static_cast<char*>(q0);
+  char* q_out = static_cast<char*>(q0) + size_t(qstride) * (T::kPacked ? 4u : 8u);
+  const bool input_active = (d.dev_final & kInputActive) != 0;
+  const bool detect_vh = !INET_EXACT_CODE && sh.detect_vh;
   for (uint32_t r = 1; !stop; ++r) {
-    RoundCtr* cur = &ctl->ctr3[set];
     c.cur = cur;
 #if INET_STAMPS
     c.round = r;
@@ -1455,10 +1461,9 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       c.ints = c.comms = 0;
       c.parked = 0;
     }
-    if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(&ctl->ctr3[set_next])[threadIdx.x] = 0;
+    if (threadIdx.x < sizeof(RoundCtr) / 4) reinterpret_cast<uint32_t*>(nxt)[threadIdx.x] = 0;
     c.dout = INET_EXACT_CODE && sh.exact ? d.deferred + (r & 1u) * d.cap_def : nullptr;
-    c.out = T::kPacked ? static_cast<void*>(static_cast<uint32_t*>(q0) + (r & 1u) * qstride)
-                       : static_cast<void*>(static_cast<uint2*>(q0) + (r & 1u) * qstride);
+    c.out = q_out;
     if (INET_EXACT_CODE && nd) {
       // equations merged last round that are still var-headed: this round's
       // communication links them (reference loop mode)
@@ -1492,8 +1497,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
         }
       }
     } else if constexpr (T::kPacked) {
-      const uint32_t* in = static_cast<const uint32_t*>(q0) + ((r - 1) & 1u) * qstride;
-      c.out = static_cast<uint32_t*>(q0) + (r & 1u) * qstride;
+      const uint32_t* in = reinterpret_cast<const uint32_t*>(q_in);
       if constexpr (kWarpRewrite) {
         for (uint32_t b = threadIdx.x & ~31u; b < n; b += blockDim.x) {
           const uint32_t i = b + lane;
@@ -1508,8 +1512,7 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
         }
       }
     } else {
-      const uint2* in = static_cast<const uint2*>(q0) + ((r - 1) & 1u) * qstride;
-      c.out = static_cast<uint2*>(q0) + (r & 1u) * qstride;
+      const uint2* in = reinterpret_cast<const uint2*>(q_in);
       if constexpr (kWarpRewrite) {
         for (uint32_t b = threadIdx.x & ~31u; b < n; b += blockDim.x) {
           const uint32_t i = b + lane;
@@ -1562,8 +1565,15 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       tot_i += k.ints;
       tot_c += k.comms;
     }
-    set = set_next;
-    set_next = set_next == 2 ? 0u : set_next + 1;
+    {
+      RoundCtr* t = cur;
+      cur = nxt;
+      nxt = old;
+      old = t;
+      char* u = q_in;
+      q_in = q_out;
+      q_out = u;
+    }
     if (per_round && threadIdx.x == 0) {
 #ifdef INET_NO_TIMER
       const unsigned long long now = 0;
@@ -1578,14 +1588,14 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     // a round that had no pairs and whose deferred equations all parked was
     // itself the reference's trailing no-op loop (exact mode: the last loop can
     // be communication only); no second trailing row then
-    const bool was_noop = (r > 1 ? n == 0 : (d.dev_final & kInputActive) == 0) && q == 0 &&
+    const bool was_noop = (r > 1 ? n == 0 : !input_active) && q == 0 &&
                           (INET_EXACT_CODE ? k.dcount : 0u) == 0;
     rounds = was_noop ? r : r + 1;
     n = q;
     nd = INET_EXACT_CODE ? k.dcount : 0u;
     if (round_failed) {
       stop = true;
-    } else if (!INET_EXACT_CODE && sh.detect_vh && k.vh) {
+    } else if (detect_vh && k.vh) {
       stop = true;  // the host reruns the net with reference-loop code
       stop_err = kNeedExact;
     } else if (was_noop) {
