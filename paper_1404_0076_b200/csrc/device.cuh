@@ -113,6 +113,7 @@ struct Traits<kTierX> : Traits<kTierG> {};
 // (Tier C reads {qcount, ints, comms, parked} of every CTA with one 16-byte
 // distributed-shared-memory load, so they lead.)
 constexpr uint32_t kErrBit = 0x80000000u;  // in qcount: a failure in this round
+constexpr uint32_t kAgentCache = 4096;     // tier M: shared-memory agent-record cache entries
 struct RoundCtr {
   uint32_t qcount;  // active pairs queued for the next round (| kErrBit on failure)
   uint32_t ints;
@@ -301,6 +302,7 @@ struct Round {
   const NetDesc* d;
   Ctl* ctl;
   uint4* agents;
+  uint4* acache;  // tier M: cache of agent records, [kAgentCache]
   uint32_t* vslot;
   Ring* aring;
   Ring* vring;
@@ -505,17 +507,33 @@ __device__ __forceinline__ uint4 unpack_agent_s(const uint2& w) {
   return make_uint4(w.x & 0xFFFFu, sext16(w.x >> 16), sext16(w.y), sext16(w.y >> 16));
 }
 
+// Tier M keeps its arena in global memory, and a record written in one round
+// is read in the next by another thread: past the round barrier that load
+// goes to L2 (~700 cycles on a narrow round's critical path,
+// profiles/r02al_round_trace.txt). Every store therefore also goes to a
+// direct-mapped shared-memory cache of records, tagged in the label word's
+// high half (label < 2^16, id < 2^16: tag = id / kAgentCache + 1, 0 = empty);
+// a load that finds its tag there does not touch global memory. The global
+// arena stays complete (write-through), so the hand-over to a cluster and the
+// host finalize read it as before.
 template <int kTier>
 __device__ __forceinline__ uint4 ld_agent(const Round<kTier>& c, uint32_t a) {
   if constexpr (kTier == kTierC) return dsmem_ld4(c.agents + (a >> c.gshift), a & (c.stride - 1));
   else if constexpr (Traits<kTier>::kCompact) return unpack_agent_s(reinterpret_cast<const uint2*>(c.agents)[a]);
-  else return c.agents[a];
+  else if constexpr (kTier == kTierM) {
+    const uint4 e = c.acache[a & (kAgentCache - 1u)];
+    if ((e.x >> 16) == (a / kAgentCache) + 1u) return make_uint4(e.x & 0xFFFFu, e.y, e.z, e.w);
+    return c.agents[a];
+  } else return c.agents[a];
 }
 template <int kTier>
 __device__ __forceinline__ void st_agent(const Round<kTier>& c, uint32_t a, const uint4& v) {
   if constexpr (kTier == kTierC) dsmem_st4(c.agents + (a >> c.gshift), a & (c.stride - 1), v);
   else if constexpr (Traits<kTier>::kCompact) reinterpret_cast<uint2*>(c.agents)[a] = pack_agent_s(v);
-  else c.agents[a] = v;
+  else if constexpr (kTier == kTierM) {
+    c.agents[a] = v;
+    c.acache[a & (kAgentCache - 1u)] = make_uint4(v.x | (((a / kAgentCache) + 1u) << 16), v.y, v.z, v.w);
+  } else c.agents[a] = v;
 }
 template <int kTier>
 __device__ __forceinline__ uint32_t exch_slot(const Round<kTier>& c, uint32_t x, uint32_t v) {
@@ -1198,6 +1216,7 @@ __device__ __forceinline__ uint32_t block_scan_flag(bool flag, uint32_t* warp_to
 //   rule table | Ctl | agent ring | var ring | [S: agents] | [S,M: slots] | [S,M: 2 queues]
 struct SmemPlan {
   uint32_t ctl_off, aring_off, vring_off, agents_off, slots_off, queue_off, env_off, cagent_off, words;
+  uint32_t acache_off;  // tier M: agent-record cache
   uint32_t outc_off, inbox_off, mbox_off;  // tier C
 };
 
@@ -1205,7 +1224,7 @@ __host__ __device__ inline uint32_t align4(uint32_t w) { return (w + 3u) & ~3u; 
 
 // Shared-memory plan (32-bit words):
 //   S: rules | Ctl | u16 rings | agents | slots | 2 packed queues
-//   M: rules | Ctl | u16 rings | slots | 2 packed queues        (agents global)
+//   M: rules | Ctl | u16 rings | slots | 2 packed queues | agent cache (agents global)
 //   G: rules | Ctl | u32 rings                                   (rest global)
 //   C: rules | Ctl | u32 rings | 3 counter sets | 3 mail counts | 3 inboxes |
 //      2x2 mailboxes | slots | 2 input queues [16][res_queue] | agents
@@ -1236,6 +1255,11 @@ __host__ __device__ inline SmemPlan plan_smem(const Shape& sh, int tier) {
   p.env_off = p.queue_off + (res_slots ? align4(2 * sh.res_queue) : 0);
   p.cagent_off = p.env_off;
   p.words = p.cagent_off;
+  p.acache_off = 0;
+  if (tier == kTierM) {
+    p.acache_off = align4(p.words);
+    p.words = p.acache_off + 4 * kAgentCache;
+  }
   return p;
 }
 
@@ -1367,6 +1391,9 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
     c.agents = d.agents;
     c.cap_agents = d.cap_agents;
   }
+  c.acache = reinterpret_cast<uint4*>(smem + plan.acache_off);
+  if constexpr (kTier == kTierM)
+    for (uint32_t i = threadIdx.x; i < kAgentCache; i += blockDim.x) c.acache[i] = make_uint4(0, 0, 0, 0);
   if constexpr (T::kSlotsSmem) {
     c.vslot = smem + plan.slots_off;
     c.cap_vars = sh.res_vars;
@@ -1448,7 +1475,15 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
   char* q_out = static_cast<char*>(q0) + size_t(qstride) * (T::kPacked ? 4u : 8u);
   const bool input_active = (d.dev_final & kInputActive) != 0;
   const bool detect_vh = !INET_EXACT_CODE && sh.detect_vh;
+#ifdef INET_TRACE
+  long long tr_top = 0;
+  uint32_t tr_items = 0;
+#endif
   for (uint32_t r = 1; !stop; ++r) {
+#ifdef INET_TRACE
+    tr_top = clock64();
+    tr_items = 0;
+#endif
     c.cur = cur;
 #if INET_STAMPS
     c.round = r;
@@ -1507,8 +1542,13 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
         }
       } else {
         for (uint32_t i = threadIdx.x; i < n && !c.failed; i += blockDim.x) {
+          INET_TR(c, 0);
           const uint32_t w = in[i];
           interact(c, w >> 16, w & 0xFFFFu);
+#ifdef INET_TRACE
+          c.tr[6] = clock64();
+          tr_items += 1;
+#endif
         }
       }
     } else {
@@ -1539,8 +1579,23 @@ __device__ void run_net(const NetDesc& d, const Shape& sh, const uint16_t* pair,
       }
     }
     INET_TMARK(c, 6);
+#ifdef INET_TRACE
+    const long long tr_arr = clock64();
+#endif
     __syncthreads();
     INET_TMARK(c, 7);
+#ifdef INET_TRACE
+    {  // development: one line per thread with pairs (and thread 0) in rounds [R0, R0 + 3)
+      const long long tr_exit = clock64();
+      if (r >= INET_TRACE_R0 && r < INET_TRACE_R0 + 3 && (tr_items || threadIdx.x == 0) && blockIdx.x == 0)
+        printf("MT r=%u t=%u items=%u n=%u start=%lld q+ag=%lld pair=%lld alloc=%lld recs=%lld exissue=%lld settle=%lld "
+               "tail=%lld arrive=%lld exit=%lld\n",
+               r, threadIdx.x, tr_items, n, tr_items ? c.tr[0] - tr_top : 0ll, tr_items ? c.tr[2] - c.tr[0] : 0ll,
+               tr_items ? c.tr[2] - c.tr[1] : 0ll, tr_items ? c.tr[3] - c.tr[2] : 0ll, tr_items ? c.tr[4] - c.tr[3] : 0ll,
+               tr_items ? c.tr[5] - c.tr[4] : 0ll, tr_items ? c.tr[6] - c.tr[5] : 0ll,
+               tr_items ? tr_arr - c.tr[6] : 0ll, tr_arr - tr_top, tr_exit - tr_top);
+    }
+#endif
     // ---- close round r (every thread, same values)
     const RoundCtr k = *cur;
     bool round_failed = (k.qcount & kErrBit) != 0;
