@@ -169,6 +169,12 @@ struct PinnedU32 {
     }
     n = want;
   }
+  void assign(const uint32_t* b, const uint32_t* e) {
+    resize(static_cast<size_t>(e - b));
+    if (e != b) std::memcpy(p, b, static_cast<size_t>(e - b) * 4);
+  }
+  uint32_t& operator[](size_t i) { return p[i]; }
+  const uint32_t& operator[](size_t i) const { return p[i]; }
   uint32_t* data() { return p; }
   const uint32_t* data() const { return p; }
   bool empty() const { return n == 0; }
@@ -185,7 +191,8 @@ struct inet_ctx {
   uint32_t n_labels = 0, n_rules = 0, smem_bytes = 0;
   // batch input (host copies)
   uint32_t n_nets = 0;
-  std::vector<uint32_t> agents, eqs, iface, n_vars;
+  PinnedU32 agents, eqs, iface;  // page-locked: the upload is an asynchronous copy
+  std::vector<uint32_t> n_vars;
   std::vector<uint64_t> agent_off, eq_off, iface_off;
   uint32_t max_in_agents = 0, max_in_eqs = 0, max_in_vars = 0;
   bool input_resident = false;
@@ -233,6 +240,8 @@ struct inet_ctx {
   bool zc_next = false;               // the next layout puts tier S results in h_zc
   bool zc_used = false;               // the last run's results are in h_zc (pitch cap_agents)
   PinnedU32 h_resid;                  // [n_nets * resid_pitch * 2]
+  PinnedU32 h_desc;                   // layout(): the descriptor table's host staging
+  PinnedU32 h_ctl;                    // the control blocks' host staging
   uint32_t agent_pitch = 0, resid_pitch = 0;
   std::vector<uint32_t> h_rounds;     // [n_nets * rows_pitch * 4]
   uint32_t rows_pitch = 1;
@@ -471,7 +480,11 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
   if (c->var_order && c->d_stamps.ensure(N * cap_vars * 8)) return INET_ERR_CUDA;
   if (c->grid_tier) CUDA_TRY(cudaMemsetAsync(c->d_gs.p, 0, sizeof(inetdev::GridState) + 4096 * 4, c->stream));
   if (c->count_rules) CUDA_TRY(cudaMemsetAsync(c->d_hist.p, 0, N * hist_stride(c) * 4, c->stream));
-  std::vector<NetDesc> desc(n);
+  // descriptors staged in page-locked memory (a pageable source would make
+  // the copy a staged, synchronous one on every launch)
+  static_assert(sizeof(NetDesc) % 4 == 0, "NetDesc words");
+  c->h_desc.resize(N * sizeof(NetDesc) / 4);
+  NetDesc* desc = reinterpret_cast<NetDesc*>(c->h_desc.data());
   for (uint32_t i = 0; i < n; ++i) {
     NetDesc& d = desc[i];
     std::memset(&d, 0, sizeof(d));
@@ -521,7 +534,7 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
       d.base_parked = c->resume.parked;
     }
   }
-  CUDA_TRY(cudaMemcpyAsync(c->d_desc.p, desc.data(), N * sizeof(NetDesc), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_desc.p, desc, N * sizeof(NetDesc), cudaMemcpyHostToDevice, c->stream));
   return INET_OK;
 }
 
@@ -847,7 +860,11 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     return false;
   };
   auto fetch_ctl = [&]() -> int {
-    CUDA_TRY(cudaMemcpy(c->ctl.data(), c->d_ctl.p, c->n_nets * sizeof(NetCtl), cudaMemcpyDeviceToHost));
+    static_assert(sizeof(NetCtl) % 4 == 0, "NetCtl words");
+    c->h_ctl.resize(size_t(c->n_nets) * sizeof(NetCtl) / 4);
+    CUDA_TRY(cudaMemcpyAsync(c->h_ctl.data(), c->d_ctl.p, c->n_nets * sizeof(NetCtl), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::memcpy(c->ctl.data(), c->h_ctl.data(), c->n_nets * sizeof(NetCtl));
     c->io_d2h += c->n_nets * sizeof(NetCtl);
     c->io_h2d += c->n_nets * sizeof(NetDesc);
     return INET_OK;
