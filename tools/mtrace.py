@@ -17,5 +17,7 @@ from inet.bench import program  # noqa: E402
 spec = {"a38": ("ackermann", (3, 8)), "a36": ("ackermann", (3, 6)), "fib18": ("fibonacci", (18,)),
         "add": ("addition", (300, 200))}[sys.argv[1]]
 p = program(spec[0])
-res = evaluate(p.build_input(*spec[1]), p.rules, EngineConfig(ctas_per_net=1, threads=int(os.environ.get("T", "256"))))
+fast = os.environ.get("FAST") == "1"  # the fast tiers (no stamps) instead of the default evaluation order
+res = evaluate(p.build_input(*spec[1]), p.rules, EngineConfig(ctas_per_net=1, threads=int(os.environ.get("T", "256")),
+                                                               reference_order=False if fast else None))
 print("interactions", res.total_interactions, "loops", len(res.loops), flush=True)
