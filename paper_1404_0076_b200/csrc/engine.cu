@@ -538,6 +538,17 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
   return INET_OK;
 }
 
+// Tier M queue (pairs per round): its round counters keep pushes and freed
+// variables in 16-bit halves of one word (device.cuh kPush2), so a round may
+// queue at most 65,535 pairs: pairs x (equations per rule + 1) must stay below
+// that (5,120 for every rule set with up to 11 equations per rule).
+uint32_t tier_m_queue(const inet_ctx* c) {
+  const uint32_t pair_words = (c->n_labels * c->n_labels + 1) / 2;
+  uint32_t max_eq = 0;
+  for (uint32_t r = 0; r < c->n_rules; ++r) max_eq = std::max(max_eq, (c->blob[4 + pair_words + r * 16] >> 8) & 0xFFu);
+  return std::min<uint32_t>(5120u, 65535u / (max_eq + 1u)) & ~3u;
+}
+
 uint32_t auto_threads(const inet_ctx* c, const inet_cfg* cfg) {
   if (cfg && cfg->threads) {
     uint32_t t = cfg->threads;
@@ -1001,7 +1012,7 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
     if (c->max_in_agents < 32768 && c->max_in_vars < 16384) {
       Shape sh = base_shape(c, max_loops);
       sh.res_vars = 14336;
-      sh.res_queue = 5120;
+      sh.res_queue = tier_m_queue(c);
       sh.ring_a = 8192;
       sh.ring_v = 8192;
       sh.promote_ints = c->promote_ints;
@@ -1069,7 +1080,7 @@ int run_once(inet_ctx* c, const inet_cfg* cfg, float* device_ms, bool fetch) {
   if (!done && !user_caps && c->n_nets <= 148 && c->max_in_agents < 32768 && c->max_in_vars < 16384) {
     Shape sh = base_shape(c, max_loops);
     sh.res_vars = 14336;
-    sh.res_queue = 5120;
+    sh.res_queue = tier_m_queue(c);
     sh.ring_a = 8192;
     sh.ring_v = 8192;
     int st = attempt_tier(kTierM, sh, 65535, sh.res_vars, 1);
