@@ -412,3 +412,28 @@ def test_symbol_only_on_a_right_hand_side():
     res = evaluate(net, rs)
     assert print_configuration(res.final) == "net C : ;"
     assert res.total_interactions == 1
+
+
+def test_rule_with_the_most_equations_single_and_batch():
+    """A rule with the most right-hand-side equations the rule compiler takes
+    (8: a variable chain and four agent pairs; tier M sizes its queue so a
+    round's pushes fit the 16-bit push counter, engine.cu tier_m_queue):
+    single net and batch equal the oracle, text, counts and rows."""
+    import sys
+
+    sys.path.insert(0, __import__("os").path.dirname(__file__))
+    import fuzz_gen as F
+
+    src = "A(a) >< B(b) => a = x1, x1 = x2, x2 = x3, x3 = b, Z = Z, Z = Z, Z = Z, Z = Z;\nZ >< Z => ;\n"
+    names = ", ".join(f"r{i}, s{i}" for i in range(300))
+    eqs = ", ".join(f"A(r{i}) = B(s{i})" for i in range(300))
+    sp = parse_program(src + f"net {names} : {eqs};")
+    orules = O.compile_golden_rules(F.to_golden(sp.rules))
+    want = O.run_config(sp.net, orules, collect=True)
+    res = evaluate(sp.net, sp.rules, EngineConfig())
+    assert res.total_interactions == want.interactions
+    assert res.total_communications == want.communications
+    assert [(s.interactions, s.communications, s.live_equations) for s in res.loops] == [tuple(r) for r in want.rows]
+    assert print_configuration(res.final) == want.printed()
+    out = evaluate_batch([sp.net] * 64, sp.rules, EngineConfig(collect_stats=False), as_text=True)
+    assert all(t == want.printed() for t in out.texts)
