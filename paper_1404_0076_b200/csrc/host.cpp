@@ -459,33 +459,16 @@ struct Printer {
     return true;
   }
 
-  // first-occurrence variable numbering, preorder (children left to right)
-  bool assign(uint32_t root, std::unordered_map<uint32_t, uint32_t>& ids) {
+  // Prints one term; a variable gets its number at its first occurrence in
+  // printing order (interface terms, then the sorted equations left to right),
+  // which is core.iter_vars' first-occurrence preorder — numbering and printing
+  // in one walk.
+  bool term(uint32_t root, std::unordered_map<uint32_t, uint32_t>& ids, std::string& out) {
     std::vector<uint32_t>& s = *st;
     s.clear();
     s.push_back(root);
     uint64_t seen = 0;
-    while (!s.empty()) {
-      const uint32_t t = s.back();
-      s.pop_back();
-      if (t == kNone) return false;
-      if (t & kVar) {
-        ids.emplace(t & ~kVar, static_cast<uint32_t>(ids.size()));
-        continue;
-      }
-      if (!agent_ok(t) || ++seen > budget) return false;
-      const uint32_t lab = ag[4 * t];
-      for (int k = int(arity[lab]) - 1; k >= 0; --k) s.push_back(ag[4 * t + 1 + k]);
-    }
-    return true;
-  }
-
-  bool term(uint32_t root, const std::unordered_map<uint32_t, uint32_t>& ids, std::string& out) {
-    std::vector<uint32_t>& s = *st;
-    s.clear();
-    s.push_back(root);
-    uint64_t seen = 0;
-    char num[16];
+    char num[12];
     while (!s.empty()) {
       const uint32_t t = s.back();
       s.pop_back();
@@ -497,10 +480,18 @@ struct Printer {
         out.push_back(',');
         continue;
       }
+      if (t == kNone) return false;
       if (t & kVar) {
+        const uint32_t next = static_cast<uint32_t>(ids.size());
+        uint32_t id = ids.emplace(t & ~kVar, next).first->second;
+        char* e = num + sizeof(num);
+        char* b = e;
+        do {
+          *--b = static_cast<char>('0' + id % 10u);
+          id /= 10u;
+        } while (id);
         out.push_back('x');
-        const int w = std::snprintf(num, sizeof(num), "%u", ids.at(t & ~kVar));
-        out.append(num, static_cast<size_t>(w));
+        out.append(b, static_cast<size_t>(e - b));
         continue;
       }
       if (!agent_ok(t) || ++seen > budget) return false;
@@ -553,10 +544,6 @@ int print_flat(const uint32_t* agents, uint32_t n_agents, const uint32_t* iface,
     return c != 0 ? c < 0 : x.b < y.b;
   });
   ids.clear();
-  for (uint32_t i = 0; i < n_iface; ++i)
-    if (!p.assign(iface[i], ids)) return INET_ERR_ARG;
-  for (const Eq& e : es)
-    if (!p.assign(e.l, ids) || !p.assign(e.r, ids)) return INET_ERR_ARG;
   out.clear();
   out.reserve(size_t(n_agents) * 3 + 16);
   out.append("net");
