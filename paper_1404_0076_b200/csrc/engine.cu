@@ -457,7 +457,7 @@ int layout(inet_ctx* c, uint32_t cap_agents, uint32_t cap_vars, uint32_t cap_que
   c->cap_rounds = cap_rounds;
   const size_t N = n;
   uint4* zc = nullptr;  // tier S results in mapped host memory (see h_zc)
-  if (c->zc_next) {
+  if (c->zc_next && N * cap_agents * 16 <= (size_t(1) << 30)) {  // (larger batches copy after the kernel)
     c->h_zc.resize(N * cap_agents * 4);
     void* dp = nullptr;
     if (c->h_zc.pinned && cudaHostGetDevicePointer(&dp, c->h_zc.data(), 0) == cudaSuccess)
